@@ -1,0 +1,136 @@
+"""Transfers, V-cycle (Alg. 1) and MG-preconditioned CG.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Transfers: prolongation = matrix of the natural embedding V_{l-1} -> V_l,
+E_ij = phi^coarse_j(x^fine_i) over interior nodes, P = kron(E,..,E) (x fastest); the
+restriction is P^T.  A_l is rediscretised on every level.
+
+V-cycle (PAPER.md:158-176 with readings Q12, Q13): at the coarsest level (N=2, one
+patch) a single smoothing step from zero; else pre-smooth, restrict the residual,
+recurse with zero guess, prolongate-add, post-smooth (reversed colour order for MVS when
+`symmetric`, reading Q11).  The FP32 cycle is the same code on float32 copies of every
+array (reading Q21): the residual is converted at entry, the correction at exit
+(PAPER.md:749).
+
+PCG: textbook preconditioned CG (Saad Alg. 9.1) in FP64, x0 = 0 (reading Q19), stop at
+||r_n|| <= rtol ||r_0|| on the recursively updated residual;
+nu = -8 / log10((||r_n||/||r_0||)^(1/n)) (reading Q7).
+"""
+import numpy as np
+import scipy.sparse as sp
+
+from .basis import Basis1D, gauss_lobatto_points
+from .operator import assemble
+from .smoothers import PatchSolvers, smooth
+from .mesh import level_cells
+
+
+def embedding_1d(k, Nc):
+    """E (n_f x n_c): coarse global basis (Nc cells) evaluated at the fine (2Nc) interior nodes."""
+    Nf = 2 * Nc
+    t = gauss_lobatto_points(k)
+    bas = Basis1D(k)
+    nf, nc = k * Nf - 1, k * Nc - 1
+    E = np.zeros((nf, nc))
+    for i in range(nf):
+        j = i + 1
+        x = (j // k + t[j % k]) / Nf
+        c = min(int(np.floor(x * Nc)), Nc - 1)
+        tl = x * Nc - c
+        vals = bas.eval(tl, 0)[:, 0]
+        for m in range(k + 1):
+            jc = c * k + m
+            if 1 <= jc <= k * Nc - 1:
+                E[i, jc - 1] += vals[m]
+    E[np.abs(E) < 1e-15] = 0.0
+    return E
+
+
+def prolongation(k, d, Nc):
+    E = sp.csr_matrix(embedding_1d(k, Nc))
+    P = E
+    for _ in range(d - 1):
+        P = sp.kron(E, P)          # kron(E_y, E_x) etc.: x fastest
+    return P.tocsr()
+
+
+class Hierarchy:
+    """Levels 1..L (N = 2^l, reading Q9) with A_l, patch solvers and P_l (coarse l-1 -> l)."""
+
+    def __init__(self, k, d, L, sigma, dtype=np.float64):
+        self.k, self.d, self.L, self.sigma = k, d, L, sigma
+        self.A, self.ps, self.P = {}, {}, {}
+        for l in range(1, L + 1):
+            N = level_cells(l)
+            self.A[l] = assemble(k, d, N, sigma)
+            self.ps[l] = PatchSolvers(k, d, N, sigma)
+            if l > 1:
+                self.P[l] = prolongation(k, d, level_cells(l - 1))
+        self.set_dtype(dtype)
+
+    def set_dtype(self, dtype):
+        """FP32 cycle: every array rounded from the FP64 values (reading Q21)."""
+        self.dtype = dtype
+        self.Ac = {l: A.astype(dtype) for l, A in self.A.items()}
+        self.Pc = {l: P.astype(dtype) for l, P in self.P.items()}
+        for ps in self.ps.values():
+            if not hasattr(ps, "groups64"):
+                ps.groups64 = ps.groups
+            ps.groups = {key: (ids, (fac[0].astype(dtype), fac[1]), At.astype(dtype))
+                         for key, (ids, fac, At) in ps.groups64.items()}
+
+
+def vcycle(h, l, x, b, kind, steps, omega, symmetric=True):
+    """MG_l(x, b) of Algorithm 1 with readings Q12/Q13/Q11."""
+    A, ps = h.Ac[l], h.ps[l]
+    if l == 1:
+        return smooth(A, ps, np.zeros_like(b), b, kind, 1, omega)
+    x = smooth(A, ps, x, b, kind, steps, omega)
+    bc = h.Pc[l].T @ (b - A @ x)
+    e = vcycle(h, l - 1, np.zeros_like(bc), bc, kind, steps, omega, symmetric)
+    x = x + h.Pc[l] @ e
+    return smooth(A, ps, x, b, kind, steps, omega, reverse=(symmetric and kind == "mvs"))
+
+
+def precondition(h, r64, kind, steps, omega, symmetric=True):
+    """z = MG_L(0, r): convert r to the cycle dtype at entry, z to FP64 at exit."""
+    rc = r64.astype(h.dtype)
+    z = vcycle(h, h.L, np.zeros_like(rc), rc, kind, steps, omega, symmetric)
+    return z.astype(np.float64)
+
+
+def pcg(A, b, prec, rtol=1e-8, max_iter=200, x0=None):
+    """Preconditioned CG (Saad Alg. 9.1).  Returns x, iterations n, residual-norm history."""
+    x = np.zeros_like(b) if x0 is None else x0.copy()
+    r = b - A @ x
+    z = prec(r)
+    p = z.copy()
+    rz = r @ z
+    hist = [np.linalg.norm(r)]
+    n = 0
+    while n < max_iter and hist[-1] > rtol * hist[0]:
+        Ap = A @ p
+        alpha = rz / (p @ Ap)
+        x = x + alpha * p
+        r = r - alpha * Ap
+        n += 1
+        hist.append(np.linalg.norm(r))
+        if hist[-1] <= rtol * hist[0]:
+            break
+        z = prec(r)
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x, n, np.array(hist)
+
+
+def fractional_iterations(hist):
+    """nu = -8 / log10(rbar), rbar = (||r_n||/||r_0||)^(1/n) (reading Q7)."""
+    n = len(hist) - 1
+    if n == 0:
+        return 0.0
+    ratio = hist[-1] / hist[0]
+    if ratio == 0.0:
+        return 0.0
+    return -8.0 / np.log10(ratio ** (1.0 / n))

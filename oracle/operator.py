@@ -1,0 +1,272 @@
+"""Assembled C0IP operator by d-dimensional quadrature (Eq. bfc0ip).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+This is the *definition* of A_ell written out: cell integrals of the full Hessian
+contraction  int_K grad^2 u : grad^2 v  (including the mixed 2 d_xy u d_xy v terms,
+PAPER.md:53, 119) plus, on every facet, the penalty, consistency and adjoint
+consistency terms  (sigma/h_e)[d_n u][d_n v] - {d_n^2 u}[d_n v] - [d_n u]{d_n^2 v}
+ with the jump/mean of PAPER.md:87-106 (one-sided on boundary
+facets, reading Q26).  It does NOT use the Kronecker form of PAPER.md:314-342; the
+Kronecker identity is a test that compares the two.
+
+Numbering: full nodes j_a = 0..kN per axis, interior index
+i_a = j_a - 1, global id sum_a i_a n^a with n = kN-1 (x fastest).
+"""
+import itertools
+import numpy as np
+import scipy.sparse as sp
+
+from .basis import Basis1D, gauss_legendre
+
+
+def _tensor(tables):
+    """kron(T_{d-1}, ..., T_0): row = local dof (x fastest), col = point (x fastest)."""
+    out = np.ones((1, 1))
+    for T in tables[::-1]:
+        out = np.kron(out, T)
+    return out
+
+
+def reference_cell_matrix(k, d, h, nq=None):
+    """(k+1)^d square matrix of sum_{a,b} int_K d_ab u d_ab v on a cube cell of width h."""
+    bas = Basis1D(k)
+    nq = nq or (k + 2)
+    t, w = gauss_legendre(nq)
+    V, D1, D2 = bas.eval(t, 0), bas.eval(t, 1) / h, bas.eval(t, 2) / h ** 2
+    W = _tensor([w[None, :]] * d).ravel() * h ** d
+    K = 0.0
+    for a in range(d):
+        for b in range(d):
+            tabs = []
+            for ax in range(d):
+                if a == b:
+                    tabs.append(D2 if ax == a else V)
+                else:
+                    tabs.append(D1 if ax in (a, b) else V)
+            H = _tensor(tabs)                      # [nl, Q]: d_ab phi_m at points
+            K = K + (H * W) @ H.T
+    return K
+
+
+def reference_face_matrix(k, d, h, axis, kind, sigma, nq=None):
+    """Face matrix for a facet perpendicular to `axis`.
+
+    kind='interior': (2 nl)^2 on [dofs of lower cell K^- | dofs of upper cell K^+].
+    kind='lower'/'upper': nl^2 on the one cell touching the boundary facet x_axis=0 / =1.
+    """
+    bas = Basis1D(k)
+    nq = nq or (k + 2)
+    t, w = gauss_legendre(nq)
+    V = bas.eval(t, 0)
+    Wf = _tensor([w[None, :]] * (d - 1)).ravel() * h ** (d - 1) if d > 1 else np.ones(1)
+
+    def trace(tn, der):
+        """[nl, Qf]: d^der/dx_axis^der phi_m at face points (normal coordinate tn)."""
+        col = bas.eval(tn, der) / h ** der           # [k+1, 1]
+        tabs = [V] * d
+        tabs = list(tabs)
+        tabs[axis] = col
+        return _tensor(tabs)
+
+    if kind == "interior":
+        Jm, Jp = trace(1.0, 1), -trace(0.0, 1)          # outward normals +e (K^-), -e (K^+)
+        Mm, Mp = 0.5 * trace(1.0, 2), 0.5 * trace(0.0, 2)
+        J = np.vstack([Jm, Jp]); Mn = np.vstack([Mm, Mp])
+    elif kind == "lower":
+        J, Mn = -trace(0.0, 1), trace(0.0, 2)
+    elif kind == "upper":
+        J, Mn = trace(1.0, 1), trace(1.0, 2)
+    else:
+        raise ValueError(kind)
+    JW, MW = J * Wf, Mn * Wf
+    return (sigma / h) * (JW @ J.T) - JW @ Mn.T - MW @ J.T
+
+
+def _local_full_ids(k, d, N, cells):
+    """[ncells, nl] full-node ids (j-numbering, nn=kN+1 per axis) of the cells' local dofs."""
+    nn = k * N + 1
+    offs = np.array(list(itertools.product(range(k + 1), repeat=d)))[:, ::-1]   # x fastest
+    j = cells[:, None, :] * k + offs[None, :, :]                                   # [nc, nl, d]
+    strides = nn ** np.arange(d)
+    return (j * strides).sum(-1)
+
+
+def assemble_full(k, d, N, sigma, cells=None):
+    """COO->CSR of the C0IP form over full nodes (boundary nodes included).
+
+    cells: optional [m, d] int array of included cells (a window); all faces whose adjacent
+    cells are all included are added.  Default: every cell (the global matrix).
+    """
+    h = 1.0 / N
+    nn = k * N + 1
+    if cells is None:
+        cells = np.array(list(itertools.product(range(N), repeat=d)))[:, ::-1]
+    cells = np.asarray(cells, dtype=np.int64)
+    inset = np.zeros((N,) * d, dtype=bool)
+    inset[tuple(cells[:, ::-1].T)] = True                # indexed [c_{d-1},...,c_0]
+    rows, cols, vals = [], [], []
+
+    def add(ids, Mat):
+        rows.append(np.repeat(ids, Mat.shape[1], axis=1).ravel())
+        cols.append(np.tile(ids, (1, Mat.shape[0])).ravel())
+        vals.append(np.broadcast_to(Mat.ravel(), (ids.shape[0], Mat.size)).ravel())
+
+    Kc = reference_cell_matrix(k, d, h)
+    ids = _local_full_ids(k, d, N, cells)
+    add(ids, Kc)
+    for a in range(d):
+        Fi = reference_face_matrix(k, d, h, a, "interior", sigma)
+        Fl = reference_face_matrix(k, d, h, a, "lower", sigma)
+        Fu = reference_face_matrix(k, d, h, a, "upper", sigma)
+        lo = cells[cells[:, a] == 0]
+        if len(lo):
+            add(_local_full_ids(k, d, N, lo), Fl)
+        up = cells[cells[:, a] == N - 1]
+        if len(up):
+            add(_local_full_ids(k, d, N, up), Fu)
+        cand = cells[cells[:, a] < N - 1]
+        nb = cand.copy(); nb[:, a] += 1
+        ok = inset[tuple(nb[:, ::-1].T)]
+        if ok.any():
+            idm = _local_full_ids(k, d, N, cand[ok]); idp = _local_full_ids(k, d, N, nb[ok])
+            add(np.hstack([idm, idp]), Fi)
+    rows = np.concatenate(rows); cols = np.concatenate(cols); vals = np.concatenate(vals)
+    return sp.csr_matrix((vals, (rows, cols)), shape=(nn ** d, nn ** d))
+
+
+def interior_full_ids(k, d, N):
+    """Full-node ids of the interior nodes, in interior (i) order, x fastest."""
+    nn = k * N + 1
+    n = k * N - 1
+    idx = np.zeros((n,) * d, dtype=np.int64)
+    strides = nn ** np.arange(d)
+    # idx[i_{d-1}, ..., i_0] = sum_a (i_a + 1) nn^a
+    for a in range(d):
+        shape = [1] * d; shape[d - 1 - a] = n
+        idx = idx + ((np.arange(n) + 1) * strides[a]).reshape(shape)
+    return idx.ravel()
+
+
+def assemble(k, d, N, sigma):
+    """A_ell over interior DoFs (CSR), boundary rows/cols eliminated (reading Q26)."""
+    Af = assemble_full(k, d, N, sigma)
+    keep = interior_full_ids(k, d, N)
+    return Af[keep][:, keep].tocsr()
+
+
+def rhs_load(k, d, N, f, nq=None):
+    """b_i = int f phi_i (Eq. bfandrhs) by tensor Gauss quadrature per cell.
+
+    f(*coords) takes d arrays of physical coordinates.  nq defaults to k+3.
+    """
+    h = 1.0 / N
+    nq = nq or (k + 3)
+    bas = Basis1D(k)
+    t, w = gauss_legendre(nq)
+    Phi = _tensor([bas.eval(t, 0)] * d)                      # [nl, Q]
+    W = _tensor([w[None, :]] * d).ravel() * h ** d
+    cells = np.array(list(itertools.product(range(N), repeat=d)))[:, ::-1]
+    tq = np.array(list(itertools.product(range(nq), repeat=d)))[:, ::-1]   # x fastest points
+    coords = [(cells[:, a][:, None] + t[tq[:, a]][None, :]) * h for a in range(d)]
+    fv = f(*coords)                                          # [ncells, Q]
+    contrib = (fv * W) @ Phi.T                               # [ncells, nl]
+    nn = k * N + 1
+    bf = np.zeros(nn ** d)
+    np.add.at(bf, _local_full_ids(k, d, N, cells).ravel(), contrib.ravel())
+    return bf[interior_full_ids(k, d, N)]
+
+
+def paper_load(d):
+    """f = Delta^2 prod sin(pi x_a) = d^2 pi^4 prod sin(pi x_a) (readings Q1, Q8)."""
+    def f(*xs):
+        out = (d * d) * np.pi ** 4
+        for x in xs:
+            out = out * np.sin(np.pi * x)
+        return out
+    return f
+
+
+def dof_coords(k, N, i):
+    """Physical coordinate of interior 1D DoF index i (node j = i+1), SURVEY.md C1."""
+    from .basis import gauss_lobatto_points
+    t = gauss_lobatto_points(k)
+    j = np.asarray(i) + 1
+    return (j // k + t[j % k]) / N
+
+
+def residual_on_box(k, d, N, sigma, x, b, box_lo, box_hi):
+    """r = b - A x on the interior-DoF box [box_lo, box_hi) (per axis, interior indices).
+
+    Assembles the form only on a window of cells around the box (every cell and facet
+    that touches a box node's basis function), so it is exact at any N.  Used for
+    sampled parity at sizes where the global CSR does not fit.
+    """
+    n = k * N - 1
+    nn = k * N + 1
+    box_lo = np.asarray(box_lo); box_hi = np.asarray(box_hi)
+    j_lo, j_hi = box_lo + 1, box_hi                          # full-node range [j_lo, j_hi]
+    c_lo = np.maximum((j_lo - 1) // k - 1, 0)                # cells touching the box nodes ...
+    c_hi = np.minimum(j_hi // k + 1, N - 1)                  # ... and their facet neighbours
+    rng = [np.arange(c_lo[a], c_hi[a] + 1) for a in range(d)]
+    cells = np.array(list(itertools.product(*rng[::-1])))[:, ::-1]
+    Af = assemble_full(k, d, N, sigma, cells)
+    # rows: box nodes (full ids); columns: every node in the window cells
+    box_axes = [np.arange(box_lo[a], box_hi[a]) for a in range(d)]
+    bi = np.array(list(itertools.product(*box_axes[::-1])))[:, ::-1]          # interior idx
+    rows_full = ((bi + 1) * nn ** np.arange(d)).sum(-1)
+    rows_int = (bi * n ** np.arange(d)).sum(-1)
+    sub = Af[rows_full].tocoo()
+    jc = np.stack([(sub.col // nn ** a) % nn for a in range(d)], -1)
+    interior = np.all((jc >= 1) & (jc <= nn - 2), axis=1)
+    ic = ((jc - 1) * n ** np.arange(d)).sum(-1)
+    Ax = np.zeros(len(rows_full))
+    np.add.at(Ax, sub.row[interior], sub.data[interior] * x[ic[interior]])
+    return (b[rows_int] - Ax), rows_int
+
+
+def energy_error(k, d, N, sigma, uh, hess_u, nq=None):
+    """Mesh-dependent energy error |u - u_h|_h of Eq. hnorm:
+
+    sum_K |u - u_h|^2_{H^2(K)} + sum_e (sigma/h_e) ||[d_n (u - u_h)]||^2_{L^2(e)}.
+    u must be in H^2_0 and smooth (no jumps, d_n u = 0 on the boundary), so the facet part
+    reduces to the jumps of u_h.  hess_u(*coords) -> array [..., d, d].
+    """
+    h = 1.0 / N
+    nq = nq or (k + 3)
+    bas = Basis1D(k)
+    t, w = gauss_legendre(nq)
+    V, D1, D2 = bas.eval(t, 0), bas.eval(t, 1) / h, bas.eval(t, 2) / h ** 2
+    W = _tensor([w[None, :]] * d).ravel() * h ** d
+    cells = np.array(list(itertools.product(range(N), repeat=d)))[:, ::-1]
+    nn = k * N + 1
+    uf = np.zeros(nn ** d)
+    uf[interior_full_ids(k, d, N)] = uh
+    U = uf[_local_full_ids(k, d, N, cells)]                         # [ncells, nl]
+    tq = np.array(list(itertools.product(range(nq), repeat=d)))[:, ::-1]
+    coords = [(cells[:, a][:, None] + t[tq[:, a]][None, :]) * h for a in range(d)]
+    Hu = hess_u(*coords)                                            # [ncells, Q, d, d]
+    bulk = 0.0
+    for a in range(d):
+        for b in range(d):
+            tabs = []
+            for ax in range(d):
+                if a == b:
+                    tabs.append(D2 if ax == a else V)
+                else:
+                    tabs.append(D1 if ax in (a, b) else V)
+            Hh = U @ _tensor(tabs)                                  # [ncells, Q]
+            bulk += (((Hu[..., a, b] - Hh) ** 2) * W).sum()
+    face = 0.0
+    for a in range(d):
+        for kind in ("interior", "lower", "upper"):
+            # penalty-only face matrix: (sigma/h) J J^T  ==  face matrix with b-terms removed
+            Fs = reference_face_matrix(k, d, h, a, kind, sigma) - reference_face_matrix(k, d, h, a, kind, 0.0)
+            if kind == "interior":
+                cm = cells[cells[:, a] < N - 1]; cp = cm.copy(); cp[:, a] += 1
+                Uf = np.hstack([uf[_local_full_ids(k, d, N, cm)], uf[_local_full_ids(k, d, N, cp)]])
+            else:
+                sel = cells[cells[:, a] == (0 if kind == "lower" else N - 1)]
+                Uf = uf[_local_full_ids(k, d, N, sel)]
+            face += np.einsum("ci,ij,cj->", Uf, Fs, Uf)
+    return np.sqrt(bulk + face)

@@ -1,0 +1,119 @@
+"""Pins for transfers, V-cycle and PCG of the oracle."""
+import numpy as np
+import pytest
+import scipy.sparse.linalg as spla
+
+from oracle.multigrid import (embedding_1d, prolongation, Hierarchy, vcycle, precondition, pcg,
+                              fractional_iterations)
+from oracle.operator import dof_coords, rhs_load, paper_load
+from oracle.mesh import level_cells
+from oracle.discretization import default_sigma
+from c0ip_inputs import uniform
+from golden_io import read_matrices
+
+
+def test_embedding_golden_appendix_A():
+    g = read_matrices("k2_N2_sigma6_1d.txt")
+    assert np.allclose(embedding_1d(2, 2), g["E"], atol=1e-15)
+
+
+@pytest.mark.parametrize("k", range(2, 8))
+def test_embedding_reproduces_polynomials(k):
+    """E maps the coarse interpolant of p in Q_k (p(0)=p(1)=0) to the fine one."""
+    Nc = 3
+    E = embedding_1d(k, Nc)
+    xc = dof_coords(k, Nc, np.arange(k * Nc - 1)); xf = dof_coords(k, 2 * Nc, np.arange(2 * k * Nc - 1))
+    for deg in range(2, k + 1):
+        p = lambda x: x * (1 - x) * (x + 0.3) ** (deg - 2)
+        assert np.abs(E @ p(xc) - p(xf)).max() < 1e-12
+
+
+def test_prolongation_restriction_adjoint():
+    """<P c, f> = <c, P^T f> and the kron order is x fastest."""
+    k, Nc = 3, 3
+    P = prolongation(k, 2, Nc)
+    c = uniform(P.shape[1], 1); f = uniform(P.shape[0], 2)
+    assert abs((P @ c) @ f - c @ (P.T @ f)) < 1e-13 * np.abs(f).sum()
+    xc = dof_coords(k, Nc, np.arange(k * Nc - 1)); xf = dof_coords(k, 2 * Nc, np.arange(2 * k * Nc - 1))
+    u = lambda x, y: x * (1 - x) * y * y * (1 - y)
+    cc = u(xc[None, :], xc[:, None]).ravel(); ff = u(xf[None, :], xf[:, None]).ravel()
+    assert np.abs(P @ cc - ff).max() < 1e-13
+
+
+@pytest.fixture(scope="module")
+def h2():
+    return Hierarchy(2, 2, 3, default_sigma(2))
+
+
+def test_vcycle_fixed_point(h2):
+    """b = A x*, x = x* -> x*."""
+    L = 3
+    xs = uniform(h2.A[L].shape[0], 5)
+    out = vcycle(h2, L, xs.copy(), h2.A[L] @ xs, "avs", 2, 0.25)
+    assert np.abs(out - xs).max() <= 1e-12 * np.abs(xs).max()
+
+
+@pytest.mark.parametrize("kind,steps,omega", [("avs", 2, 0.25), ("mvs", 1, 1.0)])
+def test_preconditioner_symmetric(h2, kind, steps, omega):
+    """Reading Q11: AVS cycle and the reversed-post-order MVS cycle are symmetric (CG-valid)."""
+    n = h2.A[3].shape[0]
+    r1, r2 = uniform(n, 11), uniform(n, 12)
+    lhs = precondition(h2, r1, kind, steps, omega) @ r2
+    rhs = r1 @ precondition(h2, r2, kind, steps, omega)
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+    assert precondition(h2, r1, kind, steps, omega) @ r1 > 0
+
+
+@pytest.mark.parametrize("nratio,n,nu", [(1e-8, 10, 10.0), (1e-4, 2, 4.0), (1e-16, 8, 4.0)])
+def test_fractional_iterations_arithmetic(nratio, n, nu):
+    """SPEC.md:480-482 (reading Q7)."""
+    hist = np.r_[1.0, np.ones(n - 1), nratio]
+    assert abs(fractional_iterations(hist) - nu) < 1e-12
+
+
+def test_cfg1_pcg_matches_direct(h2):
+    """cfg1 (2D, Q2, 8x8): MG-PCG to 1e-8 equals the dense direct solve."""
+    L = 3
+    A = h2.A[L]
+    b = rhs_load(2, 2, level_cells(L), paper_load(2))
+    x, n, hist = pcg(A, b, lambda r: precondition(h2, r, "avs", 2, 0.25))
+    xd = spla.spsolve(A.tocsc(), b)
+    assert hist[-1] <= 1e-8 * hist[0]
+    assert np.linalg.norm(x - xd) <= 1e-6 * np.linalg.norm(xd)
+    assert np.linalg.norm(b - A @ x) <= 1.0001e-8 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_mixed_precision_iterations(k):
+    """PAPER.md:747 / SPEC.md:490: FP32 cycle in FP64 CG -> same accuracy, iteration count close.
+
+    The oracle's FP32 cycle rounds the dense Cholesky factors (reading Q21); with plain
+    (non-flexible) CG this costs up to 2 iterations here."""
+    L = 4
+    h = Hierarchy(k, 2, L, default_sigma(k))
+    b = rhs_load(k, 2, level_cells(L), paper_load(2))
+    _, n64, _ = pcg(h.A[L], b, lambda r: precondition(h, r, "avs", 2, 0.25))
+    h.set_dtype(np.float32)
+    x32, n32, hist = pcg(h.A[L], b, lambda r: precondition(h, r, "avs", 2, 0.25))
+    assert abs(n32 - n64) <= 2
+    assert np.linalg.norm(b - h.A[L] @ x32) <= 1.01e-8 * np.linalg.norm(b)
+
+
+def test_two_grid_h_independent():
+    """Two-grid (exact coarse solve) iteration counts settle as h -> 0 (MG approximation +
+    smoothing property); the full V-cycle ν is recorded in DESIGN.md against Tables 2-3."""
+    from oracle.smoothers import smooth
+    k = 2
+    nus = []
+    for L in (5, 6):
+        h = Hierarchy(k, 2, L, default_sigma(k))
+        A, P = h.A[L], h.P[L]
+        lu = spla.splu(h.A[L - 1].tocsc())
+
+        def tg(r):
+            x = smooth(A, h.ps[L], np.zeros_like(r), r, "avs", 2, 0.25)
+            x = x + P @ lu.solve(P.T @ (r - A @ x))
+            return smooth(A, h.ps[L], x, r, "avs", 2, 0.25)
+        b = rhs_load(k, 2, level_cells(L), paper_load(2))
+        nus.append(fractional_iterations(pcg(A, b, tg)[2]))
+    assert abs(nus[1] - nus[0]) < 1.5 and nus[1] < 20
