@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the vertex-patch smoother hot path (arXiv 2412.05082) -- one JSON line.
+
+Workload (BASELINE.json configs[1] / SURVEY.md §8d cfg2): 2D unit square, Q_k C0IP with
+k = --degree (default 4), N_k cells per axis so that (kN-1)^2 ~ 16.7M DoFs, FP64, one B200.
+A *step* is one additive vertex-patch smoothing application: residual
+r = b - A x with the matrix-free C0IP operator, per-patch gather, approximate FDM local solve
+(S^T, Lambda^-1, S per axis) and scatter-add, all on device.
+
+value  = DoFs x ranks / (max over ranks of the device time per step), GDoF/s.
+e2e    = the same step through the C ABI with host buffers: x, b copied from pinned host
+         memory to the device and x' back, inside the timed region.
+Extras: matvec GDoF/s on the same mesh, per-kernel roofline of the dominant kernel, an MG-PCG
+time-to-solve (FP64 vs FP32 V-cycle, nested mesh) and the CPU oracle baseline.
+
+Multi-GPU (torchrun, --gpus N): every rank runs its own copy of the workload (replicas, no
+data-path collective yet), timing is the max over ranks.
+--impl reference: times the CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from c0ip_inputs import CFG2_CELLS, random_xb  # noqa: E402
+
+METRIC = "smoother & C0IP matvec GDoF/s; MG-PCG time-to-solve, FP64 vs mixed precision"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("hbm_gbs", 6650.0), d.get("sm_max_mhz", 1965.0), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+def fp64_peak_tflops(mhz):
+    """B200: 148 SMs x 64 FP64 FMA/clk/SM x 2 flop, at the given clock."""
+    return 148 * 64 * 2 * mhz * 1e6 / 1e12
+
+
+def fp32_peak_tflops(mhz):
+    return 148 * 128 * 2 * mhz * 1e6 / 1e12
+
+
+# algorithmic work per DoF of the fused 2D kernels; FP64 bytes
+def flops_residual_2d(k):
+    # x-stage B^ (avg 3k+2 nonzeros), L^, M^ (avg k+2) and the same on the y-stage, 2 flop/MAC
+    per = (3 * k + 2) + 2 * (k + 2)
+    return 2.0 * 2 * per
+
+
+def flops_fdm_2d(k):
+    np_ = 2 * k - 1
+    return 2.0 * (np_ * np_ / k + 2.0 * np_ ** 3 / k ** 2 + (2 * k - 1) * np_ / k)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.idx = device_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_oracle_sample(k, seconds_target=15.0):
+    """Time the CPU oracle (as it stands) on an oracle-size twin of the workload: 2D, same k,
+    ~0.26-1M DoFs, one AVS step (CSR residual + dense surrogate patch solves).  Assembly excluded."""
+    import numpy as np
+    from oracle.operator import assemble
+    from oracle.smoothers import PatchSolvers, avs_step
+    from oracle.discretization import default_sigma
+    N = {2: 256, 3: 170, 4: 128, 5: 102, 6: 85, 7: 73}[k]
+    s = default_sigma(k)
+    A = assemble(k, 2, N, s)
+    ps = PatchSolvers(k, 2, N, s)
+    x, b = random_xb(k, 2, N)
+    ndofs = len(x)
+    reps, t_total = 0, 0.0
+    while t_total < seconds_target and reps < 50:
+        t0 = time.perf_counter()
+        avs_step(A, ps, x, b, 0.25)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return {"value": ndofs * reps / t_total / 1e9, "unit": "GDoF/s", "cores": cores, "kind": "oracle",
+            "sample": f"2D k={k} N={N} ({ndofs} DoFs), {reps} AVS step(s) in {t_total:.1f}s, CSR assembly excluded",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and rank != 0:
+        return
+    k = args.degree
+    cb = cpu_oracle_sample(k, seconds_target=max(5.0, 20.0 / max(1, args.steps + args.warmup)))
+    line = {"metric": METRIC, "value": cb["value"], "unit": "GDoF/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg2: 2D unit square Q{k} C0IP, one AVS smoothing step (oracle-size twin)",
+                       "degree": k},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def traffic_from_profiles(kernel_key):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(kernel_key)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--degree", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-pcg", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    from paper_2412_05082_b200 import api
+
+    k = args.degree
+    N = CFG2_CELLS[k]
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    ctx = api.Context(2, k, 3, cells_override=N, device=local)
+    L = 3
+    ndofs = ctx.n_dofs(L)
+    x0, b0 = random_xb(k, 2, N)
+    x = torch.tensor(x0, device="cuda", dtype=dt)
+    b = torch.tensor(b0, device="cuda", dtype=dt)
+    r = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+    omega = 0.25
+
+    def step():
+        ctx.smooth(L, "avs", 1, omega, b, x)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    lc0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        t_step_ms = ev0.elapsed_time(ev1) / args.steps
+        launches = (ctx.launch_count() - lc0)
+        # per-kernel timing (same stream): residual (apply2d) and FDM apply (fdm2d) separately
+        for _ in range(3):
+            ctx.residual(L, b, x, r)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.residual(L, b, x, r)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_res_ms = e0.elapsed_time(e1) / args.steps
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.apply(L, x, r)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_mv_ms = e0.elapsed_time(e1) / args.steps
+    barrier(world)
+    t_step_ms = max_over_ranks(t_step_ms, world)
+    clocks = clk.summary()
+
+    # e2e through the C ABI with host buffers (pinned), copies inside the timed region
+    xh = torch.tensor(x0, dtype=dt).pin_memory()
+    bh = torch.tensor(b0, dtype=dt).pin_memory()
+    outh = torch.empty_like(xh).pin_memory()
+    xd, bd = torch.empty_like(x), torch.empty_like(b)
+
+    def e2e_step():
+        xd.copy_(xh, non_blocking=True)
+        bd.copy_(bh, non_blocking=True)
+        ctx.smooth(L, "avs", 1, omega, bd, xd)
+        outh.copy_(xd, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+
+    esz = 8 if dt == torch.float64 else 4
+    hbm, mhz, peak_src = peaks()
+    clk_mhz = clocks.get("sm_mhz") or mhz
+    t_fdm_ms = max(t_step_ms - t_res_ms, 1e-9)
+    # dominant kernel of the step and its roofline (algorithmic work / live CUDA-event time)
+    kern = "fdm2d" if t_fdm_ms >= t_res_ms else "apply2d"
+    t_k = t_fdm_ms if kern == "fdm2d" else t_res_ms
+    flop = (flops_fdm_2d(k) if kern == "fdm2d" else flops_residual_2d(k)) * ndofs
+    byts = 3 * esz * ndofs
+    peak_alu = fp64_peak_tflops(clk_mhz) if esz == 8 else fp32_peak_tflops(clk_mhz)
+    ach_tf = flop / (t_k * 1e-3) / 1e12
+    ach_gb = byts / (t_k * 1e-3) / 1e9
+    f_alu, f_hbm = ach_tf / peak_alu, ach_gb / hbm
+    if f_alu >= f_hbm:
+        roof = {"bound": "alu", "achieved": round(ach_tf, 3), "peak": round(peak_alu, 2), "unit": "TFLOP/s",
+                "frac": round(f_alu, 4)}
+        alt = {"bound": "hbm", "achieved": round(ach_gb, 1), "peak": hbm, "unit": "GB/s", "frac": round(f_hbm, 4)}
+    else:
+        roof = {"bound": "hbm", "achieved": round(ach_gb, 1), "peak": hbm, "unit": "GB/s", "frac": round(f_hbm, 4)}
+        alt = {"bound": "alu", "achieved": round(ach_tf, 3), "peak": round(peak_alu, 2), "unit": "TFLOP/s",
+               "frac": round(f_alu, 4)}
+    roof["kernel"] = kern
+    roof["traffic"] = traffic_from_profiles(f"{kern}_k{k}_{args.dtype}")
+    roof["peak_source"] = f"hbm {peak_src} (MEASURED_PEAKS.json); alu derived 148x{64 if esz == 8 else 128}x2 flop/clk at {clk_mhz:.0f} MHz (DESIGN.md)"
+    roof["alt"] = alt
+    roof["launch_ms"] = round(t_k, 4)
+
+    value = ndofs * world / (t_step_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t_step_ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": f"cfg2: 2D unit square, Q{k} C0IP, N={N} cells/axis ({ndofs} DoFs), one additive "
+                               f"vertex-patch smoothing step (atomic-free gather AVS, omega=1/4)",
+                   "degree": k, "cells": N, "dofs_per_gpu": ndofs,
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (x, b, r = 3 x %.0f MB)" % (ndofs * esz / 1e6)},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "e2e": {"value": round(ndofs * world / (t_e2e_ms * 1e-3) / 1e9, 3), "unit": "GDoF/s",
+                "h2d_bytes_per_step": 2 * ndofs * esz, "d2h_bytes_per_step": ndofs * esz},
+        "roofline": roof,
+        "matvec": {"value": round(ndofs * world / (t_mv_ms * 1e-3) / 1e9, 3), "unit": "GDoF/s",
+                   "ms": round(t_mv_ms, 4)},
+        "residual_ms": round(t_res_ms, 4), "fdm_ms": round(t_fdm_ms, 4),
+    }
+
+    if not args.no_pcg:
+        # MG-PCG time-to-solve on the nested mesh N = 2^L of similar size
+        Lp = {2: 11, 3: 10, 4: 10, 5: 9, 6: 9, 7: 9}[k]
+        ctx.close()
+        cp = api.Context(2, k, Lp, device=local)
+        bb = cp.rhs(Lp)
+        res = {}
+        for name, cdt in (("fp64", torch.float64), ("mixed", torch.float32)):
+            mg = api.MG("avs", 2, 0.25, cycle_dtype=cdt)
+            cp.pcg(mg, bb, max_iter=3)            # warm-up (allocations, first launches)
+            torch.cuda.synchronize()
+            xs, rep, hist = cp.pcg(mg, bb)
+            res[name] = {"seconds": round(rep["seconds"], 4), "iterations": rep["iterations"],
+                         "nu": round(rep["nu"], 2), "converged": rep["converged"]}
+        res["dofs"] = cp.n_dofs(Lp)
+        res["config"] = f"2D Q{k}, L={Lp} (N={2 ** Lp}), AVS 2+2 steps omega=1/4, CG rtol 1e-8, x0=0, paper load"
+        res["mixed_speedup"] = round(res["fp64"]["seconds"] / res["mixed"]["seconds"], 3)
+        line["pcg"] = res
+        cp.close()
+    else:
+        ctx.close()
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_oracle_sample(k)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,169 @@
+/* c0ip.h -- C ABI of the B200 vertex-patch Schwarz smoother for the C0 interior penalty (C0IP)
+ * biharmonic discretisation on Cartesian meshes (arXiv 2412.05082).
+ *
+ * Citations are PAPER.md line numbers (section / equation / algorithm) of the paper text
+ * shipped with the reference; "reading Qn" refers to the ambiguity ledger in DESIGN.md
+ * (SURVEY.md §8c).
+ *
+ * General conventions
+ *  - Every call returns c0ip_status.  Nothing aborts or throws across the ABI.  On a non-OK
+ *    status, c0ip_last_error() returns a thread-local message.
+ *  - Argument errors (null pointers, level/colour/variant out of range, dim not 2/3, degree
+ *    not in [2,7], unsupported dtype) are detected synchronously and return C0IP_ERR_ARG
+ *    without side effects.
+ *  - Device vectors: caller-owned device pointers (e.g. torch tensors' data_ptr), contiguous,
+ *    length n_dofs(level) = (k N - 1)^d, lexicographic with x fastest (reading C1), element
+ *    type given by the dtype argument (C0IP_F64 -> double, C0IP_F32 -> float).  Host vectors
+ *    are only used where the signature says "host".
+ *  - Streams: device ops are enqueued on the given cudaStream_t (passed as void*, NULL = legacy
+ *    default stream) and do not synchronise.  c0ip_pcg synchronises once per iteration.
+ *  - Asynchronous CUDA faults are reported as C0IP_ERR_CUDA by the call that detects them.
+ *  - Ownership: the context owns every table (1D operators, FDM factors, transfer bands,
+ *    colour lists) and all workspaces; it never retains a caller pointer after return.
+ *  - Concurrency: one context per host thread / stream at a time.
+ *  - Levels: level l has N = 2^l cells per axis, l = 1..finest_level (reading Q9; level 1 is the
+ *    2^d-cell mesh with one vertex patch).  If cells_override > 0 the context
+ *    has the single level `finest_level` with N = cells_override (throughput runs; no MG).
+ */
+#ifndef C0IP_H
+#define C0IP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct c0ip_ctx_s* c0ip_ctx;
+
+typedef enum {
+  C0IP_OK = 0,
+  C0IP_ERR_ARG = 1,
+  C0IP_ERR_STATE = 2,
+  C0IP_ERR_COERCIVITY = 3,
+  C0IP_ERR_OOM = 4,
+  C0IP_ERR_CUDA = 5,
+  C0IP_ERR_NCCL = 6
+} c0ip_status;
+
+typedef enum { C0IP_F64 = 0, C0IP_F32 = 1 } c0ip_dtype;
+
+/* Smoother realisations:
+ *  AVS_ATOMIC        additive, x += w sum_v R_v^T A~_v^{-1} R_v r with global atomics (paper's "atomic AVS")
+ *  AVS_DETERMINISTIC additive, gather formulation: every DoF sums its <= 2^d patch corrections in a
+ *                    fixed order (no atomics; run-to-run bitwise reproducible)
+ *  AVS_COLORED       additive, writes serialised over the 2^d non-overlapping parity classes ("colored AVS")
+ *  MVS               coloured multiplicative, residual recomputed per colour        */
+typedef enum {
+  C0IP_AVS_ATOMIC = 0,
+  C0IP_AVS_DETERMINISTIC = 1,
+  C0IP_AVS_COLORED = 2,
+  C0IP_MVS = 3
+} c0ip_smoother;
+
+/* Kernel path selection (testing): AUTO picks the fused tile kernels when the level supports
+ * them and the generic per-axis kernels otherwise (coarse levels); GENERIC forces the latter. */
+typedef enum { C0IP_PATH_AUTO = 0, C0IP_PATH_GENERIC = 1 } c0ip_path;
+
+typedef struct {
+  int32_t dim;             /* 2 | 3                                             */
+  int32_t degree;          /* k in [2,7] (Q_k)                                    */
+  int32_t finest_level;    /* L >= 1: levels 1..L, N_l = 2^l (reading Q9)                      */
+  int64_t cells_override;  /* 0, or N for one non-nested level (throughput runs)              */
+  double penalty_scale;    /* sigma = penalty_scale * k (k+1) (reading Q4); 0 -> 1 */
+  int32_t device;          /* CUDA device ordinal                                              */
+} c0ip_config;
+
+/* Build maps, 1D operators, FDM factors per level and axis variant in FP64
+ * and FP32, transfer bands and workspaces.
+ * Errors: ARG (bad config), COERCIVITY (1D B or a patch block not SPD: sigma too small,
+ * PAPER.md:134-142), OOM, CUDA.  *out is set only on success. */
+c0ip_status c0ip_create(const c0ip_config* cfg, c0ip_ctx* out);
+c0ip_status c0ip_destroy(c0ip_ctx ctx);
+const char* c0ip_last_error(void);
+c0ip_status c0ip_set_path(c0ip_ctx ctx, c0ip_path path);
+
+/* Level geometry.  n_dofs = (kN-1)^d, n_1d = kN-1, cells = N, n_patches = (N-1)^d,
+ * n_colors = 2^(d+1).  Any output pointer may be NULL. */
+c0ip_status c0ip_level_info(c0ip_ctx ctx, int32_t level, int64_t* n_dofs, int64_t* n_1d,
+                            int64_t* cells, int64_t* n_patches, int32_t* n_colors);
+
+/* R_v of PAPER.md:206: global DoF ids (host int64 array of length (2k-1)^d, patch-local x fastest)
+ * of patch `patch` (id = sum_a (v_a-1)(N-1)^a, reading C2). */
+c0ip_status c0ip_patch_dofs(c0ip_ctx ctx, int32_t level, int64_t patch, int64_t* out);
+
+/* Patches of colour `color` (0..2^(d+1)-1, reading C3: 2 * parity class + red-black key,
+ * PAPER.md:226-227), ascending patch id, into host array out[cap]; *count = colour size.
+ * out may be NULL to query the count.  ARG if cap < count and out != NULL. */
+c0ip_status c0ip_color_patches(c0ip_ctx ctx, int32_t level, int32_t color, int64_t* out,
+                               int64_t cap, int64_t* count);
+
+/* FDM factors of axis variant (0 left v=1, 1 interior, 2 right v=N-1, 3 both N=2) on `level`:
+ * S (host, (2k-1)^2 row-major, column i = i-th generalized eigenvector, S^T M_v S = I) and
+ * lambda (host, 2k-1, ascending) of B_v S = M_v S Lambda (reading Q6).
+ * STATE if the variant does not exist on this level. */
+c0ip_status c0ip_get_fdm(c0ip_ctx ctx, int32_t level, int32_t variant, double* S, double* lambda);
+
+/* Global 1D matrices M, L, B of `level` as dense host arrays n_1d x n_1d
+ * (row-major; any pointer may be NULL).  ARG if n_1d > 4096. */
+c0ip_status c0ip_get_matrices_1d(c0ip_ctx ctx, int32_t level, double* M, double* L, double* B);
+
+/* b_i = int f phi_i for the paper load f = d^2 pi^4 prod sin(pi x_a) (readings Q1, Q8),
+ * Gauss quadrature with k+3 points per cell and axis.  b: device FP64, length n_dofs. */
+c0ip_status c0ip_rhs(c0ip_ctx ctx, int32_t level, double* b, void* stream);
+
+/* y = A x with the matrix-free C0IP operator (Eqs. c0iptensorvp(3D)). */
+c0ip_status c0ip_apply(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, const void* x, void* y,
+                       void* stream);
+/* r = b - A x. */
+c0ip_status c0ip_residual(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, const void* b,
+                          const void* x, void* r, void* stream);
+
+/* `steps` applications of the smoother with the separable FDM local solver
+ * A~_v^{-1} (Eq. localsolverbila) and damping omega; x is updated in place.
+ * reverse_colors = 1 processes MVS colours in descending order (symmetric post-smoother,
+ * reading Q11); ignored for AVS.  ARG for steps < 0 or bad smoother. */
+c0ip_status c0ip_smooth(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, c0ip_smoother sm,
+                        int32_t steps, double omega, int32_t reverse_colors, const void* b,
+                        void* x, void* stream);
+
+/* coarse = P^T fine (restriction), fine_level >= 2.  coarse has n_dofs(fine_level-1). */
+c0ip_status c0ip_restrict(c0ip_ctx ctx, int32_t fine_level, c0ip_dtype dt, const void* fine,
+                          void* coarse, void* stream);
+/* fine += P coarse (prolongation = natural embedding). */
+c0ip_status c0ip_prolongate_add(c0ip_ctx ctx, int32_t fine_level, c0ip_dtype dt,
+                                const void* coarse, void* fine, void* stream);
+
+typedef struct {
+  c0ip_smoother smoother;
+  int32_t steps;           /* pre- and post-smoothing steps                    */
+  double omega;            /* damping                             */
+  int32_t symmetric;       /* MVS: post-smoothing in reversed colour order (reading Q11)        */
+  c0ip_dtype cycle_dtype;  /* F32: V-cycle entirely in single precision          */
+} c0ip_mg_config;
+
+/* z = MG_L(0, r) (Algorithm 1, PAPER.md:158-176 with readings Q12, Q13): r, z device FP64 of the
+ * finest level; with cycle_dtype F32, r is converted at entry and z at exit.
+ * STATE if the context has a single (override) level. */
+c0ip_status c0ip_vcycle(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* r, double* z,
+                        void* stream);
+
+typedef struct {
+  int32_t iterations, converged;
+  double r0, rn, nu, seconds;
+} c0ip_report;
+
+/* MG-preconditioned CG in FP64: x (device FP64, in: x0, out: solution),
+ * b device FP64.  Stops when ||r_n|| <= rtol ||r_0|| (recursively updated residual) or after
+ * max_iter iterations (not an error: converged = 0).  nu = -8/log10((r_n/r_0)^(1/n)) (reading Q7).
+ * res_history: optional host array of max_iter+1 doubles (||r_0||..||r_n||). */
+c0ip_status c0ip_pcg(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, double* x,
+                     double rtol, int32_t max_iter, c0ip_report* rep, double* res_history,
+                     void* stream);
+
+/* Number of kernels this context has launched since creation (for the bench's gpu_launches). */
+c0ip_status c0ip_launch_count(c0ip_ctx ctx, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* C0IP_H */

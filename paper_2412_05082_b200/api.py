@@ -1,0 +1,159 @@
+"""Thin Python binding over the C ABI (include/c0ip.h): torch tensors in, device pointers out.
+
+Every computation runs in the CUDA library; this module only marshals arguments.
+PyTorch provides device memory and the current stream.
+"""
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+_DT = {torch.float64: L.F64, torch.float32: L.F32}
+SMOOTHERS = {"avs_atomic": L.AVS_ATOMIC, "avs": L.AVS_DETERMINISTIC, "avs_det": L.AVS_DETERMINISTIC,
+             "avs_colored": L.AVS_COLORED, "mvs": L.MVS}
+
+
+def _ptr(t):
+    if not t.is_cuda:
+        raise ValueError("tensor must be on a CUDA device")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dtype(t):
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise ValueError(f"unsupported dtype {t.dtype}") from None
+
+
+class MG:
+    """c0ip_mg_config: smoother, steps, omega, symmetric, cycle dtype (torch.float64/float32)."""
+
+    def __init__(self, smoother="avs", steps=2, omega=0.25, symmetric=True, cycle_dtype=torch.float64):
+        self.c = L.MgConfig(SMOOTHERS[smoother] if isinstance(smoother, str) else int(smoother), int(steps),
+                            float(omega), int(bool(symmetric)), _DT[cycle_dtype])
+
+
+class Context:
+    def __init__(self, dim, degree, finest_level, cells_override=0, penalty_scale=1.0, device=0):
+        self._lib = L.load()
+        cfg = L.Config(int(dim), int(degree), int(finest_level), int(cells_override), float(penalty_scale),
+                       int(device))
+        h = C.c_void_p()
+        L.check(self._lib.c0ip_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.dim, self.degree = int(dim), int(degree)
+        self.finest_level = int(finest_level)
+        self.device = torch.device("cuda", int(device))
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self._lib.c0ip_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ host-side maps
+    def set_path(self, generic):
+        L.check(self._lib.c0ip_set_path(self.h, L.PATH_GENERIC if generic else L.PATH_AUTO))
+
+    def level_info(self, level):
+        nd, n1, nc, npch = (C.c_int64() for _ in range(4))
+        ncol = C.c_int32()
+        L.check(self._lib.c0ip_level_info(self.h, level, C.byref(nd), C.byref(n1), C.byref(nc), C.byref(npch),
+                                          C.byref(ncol)))
+        return dict(n_dofs=nd.value, n_1d=n1.value, cells=nc.value, n_patches=npch.value, n_colors=ncol.value)
+
+    def patch_dofs(self, level, patch):
+        out = np.empty((2 * self.degree - 1) ** self.dim, dtype=np.int64)
+        L.check(self._lib.c0ip_patch_dofs(self.h, level, patch, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def color_patches(self, level, color):
+        cnt = C.c_int64()
+        L.check(self._lib.c0ip_color_patches(self.h, level, color, None, 0, C.byref(cnt)))
+        out = np.empty(cnt.value, dtype=np.int64)
+        L.check(self._lib.c0ip_color_patches(self.h, level, color, out.ctypes.data_as(C.c_void_p), cnt.value,
+                                             C.byref(cnt)))
+        return out
+
+    def fdm(self, level, variant):
+        np_ = 2 * self.degree - 1
+        S = np.empty((np_, np_)); lam = np.empty(np_)
+        L.check(self._lib.c0ip_get_fdm(self.h, level, variant, S.ctypes.data_as(C.c_void_p),
+                                       lam.ctypes.data_as(C.c_void_p)))
+        return S, lam
+
+    def matrices_1d(self, level):
+        n = self.level_info(level)["n_1d"]
+        M, Lm, B = (np.empty((n, n)) for _ in range(3))
+        L.check(self._lib.c0ip_get_matrices_1d(self.h, level, *(X.ctypes.data_as(C.c_void_p) for X in (M, Lm, B))))
+        return M, Lm, B
+
+    def launch_count(self):
+        c = C.c_int64()
+        L.check(self._lib.c0ip_launch_count(self.h, C.byref(c)))
+        return c.value
+
+    # ------------------------------------------------------------------ device ops
+    def n_dofs(self, level):
+        return self.level_info(level)["n_dofs"]
+
+    def rhs(self, level):
+        b = torch.empty(self.n_dofs(level), dtype=torch.float64, device=self.device)
+        L.check(self._lib.c0ip_rhs(self.h, level, _ptr(b), _stream()))
+        return b
+
+    def apply(self, level, x, y=None):
+        y = torch.empty_like(x) if y is None else y
+        L.check(self._lib.c0ip_apply(self.h, level, _dtype(x), _ptr(x), _ptr(y), _stream()))
+        return y
+
+    def residual(self, level, b, x, r=None):
+        r = torch.empty_like(x) if r is None else r
+        L.check(self._lib.c0ip_residual(self.h, level, _dtype(x), _ptr(b), _ptr(x), _ptr(r), _stream()))
+        return r
+
+    def smooth(self, level, smoother, steps, omega, b, x, reverse=False):
+        sm = SMOOTHERS[smoother] if isinstance(smoother, str) else int(smoother)
+        L.check(self._lib.c0ip_smooth(self.h, level, _dtype(x), sm, int(steps), float(omega), int(bool(reverse)),
+                                      _ptr(b), _ptr(x), _stream()))
+        return x
+
+    def restrict(self, fine_level, fine, coarse=None):
+        if coarse is None:
+            coarse = torch.empty(self.n_dofs(fine_level - 1), dtype=fine.dtype, device=fine.device)
+        L.check(self._lib.c0ip_restrict(self.h, fine_level, _dtype(fine), _ptr(fine), _ptr(coarse), _stream()))
+        return coarse
+
+    def prolongate_add(self, fine_level, coarse, fine):
+        L.check(self._lib.c0ip_prolongate_add(self.h, fine_level, _dtype(fine), _ptr(coarse), _ptr(fine),
+                                              _stream()))
+        return fine
+
+    def vcycle(self, mg, r, z=None):
+        z = torch.empty_like(r) if z is None else z
+        L.check(self._lib.c0ip_vcycle(self.h, C.byref(mg.c), _ptr(r), _ptr(z), _stream()))
+        return z
+
+    def pcg(self, mg, b, x=None, rtol=1e-8, max_iter=200):
+        x = torch.zeros_like(b) if x is None else x
+        rep = L.Report()
+        hist = np.zeros(max_iter + 1)
+        L.check(self._lib.c0ip_pcg(self.h, C.byref(mg.c), _ptr(b), _ptr(x), float(rtol), int(max_iter),
+                                   C.byref(rep), hist.ctypes.data_as(C.c_void_p), _stream()))
+        report = dict(iterations=rep.iterations, converged=bool(rep.converged), r0=rep.r0, rn=rep.rn, nu=rep.nu,
+                      seconds=rep.seconds)
+        return x, report, hist[: rep.iterations + 1]

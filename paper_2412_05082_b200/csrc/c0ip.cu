@@ -1,0 +1,861 @@
+// C ABI implementation: context, setup upload, operator / smoother / transfer dispatch,
+// V-cycle (Algorithm 1) and MG-preconditioned CG.  See include/c0ip.h for the contract.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/c0ip.h"
+#include "generic_kernels.cuh"
+#include "fused_dispatch.hpp"
+#include "host_setup.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+c0ip_status fail(c0ip_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+struct CudaError {
+  cudaError_t e;
+  const char* where;
+};
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess) throw CudaError{e_, #call};                                   \
+  } while (0)
+
+template <typename T>
+struct DevArr {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (p && n >= count) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count == 0) return;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw CudaError{e, "cudaMalloc"};
+    }
+    n = count;
+  }
+  void upload(const std::vector<T>& h) {
+    alloc(h.size());
+    if (!h.empty()) CK(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+template <typename T>
+std::vector<T> cast_vec(const std::vector<double>& v) {
+  return std::vector<T>(v.begin(), v.end());
+}
+
+template <typename T>
+struct Tables {
+  DevArr<T> M, L, B;                  // square bands (scaled to h), n x (4k+1)
+  DevArr<T> E, Et;                    // transfer bands (this level = fine)
+  DevArr<T> S[4], lam[4];
+  // per-dtype workspaces
+  DevArr<T> tmp[6];
+  DevArr<T> sres;                     // smoother residual
+  DevArr<T> vx, vb, vr;               // V-cycle vectors
+};
+
+struct Level {
+  int l = 0;
+  int64_t N = 0, n = 0, ndofs = 0, npatch = 0;
+  double h = 0;
+  c0ip::Band M, L, B;                 // host, scaled to h
+  c0ip::Fdm fdm;                      // host, scaled
+  c0ip::RectBand E, Et;               // transfer from level l-1 (host)
+  DevArr<int64_t> Elo, Etlo;
+  Tables<double> t64;
+  Tables<float> t32;
+  std::vector<int32_t> colors_h;      // concatenated colour lists
+  std::vector<int64_t> color_off;     // n_colors + 1
+  std::vector<int32_t> parity_h;      // concatenated parity-class lists (2^d)
+  std::vector<int64_t> parity_off;
+  DevArr<int32_t> colors_d, parity_d;
+  std::unique_ptr<c0ip::FusedLevel, c0ip::FusedLevelDeleter> fused;
+};
+
+}  // namespace
+
+struct c0ip_ctx_s {
+  c0ip_config cfg{};
+  int d = 2, k = 2;
+  double sigma = 0;
+  int lmin = 1, lmax = 1;
+  c0ip_path path = C0IP_PATH_AUTO;
+  c0ip::RefData ref;
+  std::vector<Level> levels;          // index = level number (entries < lmin unused)
+  int64_t launches = 0;
+  DevArr<double> pcg_r, pcg_z, pcg_p, pcg_Ap, dot_part, dot_out;
+  double* dot_host = nullptr;
+  ~c0ip_ctx_s() {
+    for (auto& L : levels) {
+      for (auto* t : {&L.t64.M, &L.t64.L, &L.t64.B, &L.t64.E, &L.t64.Et, &L.t64.sres, &L.t64.vx,
+                      &L.t64.vb, &L.t64.vr})
+        t->free();
+      for (auto* t : {&L.t32.M, &L.t32.L, &L.t32.B, &L.t32.E, &L.t32.Et, &L.t32.sres, &L.t32.vx,
+                      &L.t32.vb, &L.t32.vr})
+        t->free();
+      for (int i = 0; i < 6; ++i) { L.t64.tmp[i].free(); L.t32.tmp[i].free(); }
+      for (int i = 0; i < 4; ++i) { L.t64.S[i].free(); L.t64.lam[i].free(); L.t32.S[i].free(); L.t32.lam[i].free(); }
+      L.Elo.free(); L.Etlo.free(); L.colors_d.free(); L.parity_d.free();
+      L.fused.reset();
+    }
+    pcg_r.free(); pcg_z.free(); pcg_p.free(); pcg_Ap.free(); dot_part.free(); dot_out.free();
+    if (dot_host) cudaFreeHost(dot_host);
+  }
+};
+
+namespace {
+
+int ipow(int b, int e) {
+  int r = 1;
+  while (e--) r *= b;
+  return r;
+}
+
+int color_of(const int64_t* v, int d) {
+  // reading C3: 2 * parity class + red-black key
+  int parity = 0;
+  int64_t rb = 0;
+  for (int a = 0; a < d; ++a) {
+    parity |= int(v[a] % 2) << a;
+    rb += v[a] / 2;
+  }
+  return 2 * parity + int(rb % 2);
+}
+
+template <typename T>
+Tables<T>& tab(Level& L);
+template <>
+Tables<double>& tab<double>(Level& L) { return L.t64; }
+template <>
+Tables<float>& tab<float>(Level& L) { return L.t32; }
+
+dim3 grid_for(int64_t total, int block = 256) {
+  int64_t g = (total + block - 1) / block;
+  g = std::max<int64_t>(1, std::min<int64_t>(g, 148 * 32));
+  return dim3((unsigned)g);
+}
+
+template <typename T>
+c0ip::LineOp<T> square_op(const DevArr<T>& band, int k, int64_t n) {
+  c0ip::LineOp<T> op;
+  op.v = band.p;
+  op.lo = nullptr;
+  op.width = 4 * k + 1;
+  op.hw = 2 * k;
+  op.n_in = n;
+  return op;
+}
+
+template <typename T>
+void launch_axis(c0ip_ctx ctx, const c0ip::AxisArgs<T>& a, cudaStream_t st) {
+  int64_t total = a.dims[0] * a.dims[1] * a.dims[2];
+  c0ip::axis_apply_kernel<T><<<grid_for(total), 256, 0, st>>>(a);
+  ctx->launches++;
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+c0ip::AxisArgs<T> axis_args(int64_t n0, int64_t n1, int64_t n2, int axis, T* out) {
+  c0ip::AxisArgs<T> a{};
+  a.dims[0] = n0; a.dims[1] = n1; a.dims[2] = n2;
+  a.axis = axis;
+  a.nterms = 0;
+  a.z = nullptr;
+  a.gamma = 0;
+  a.beta = 0;
+  a.out = out;
+  return a;
+}
+
+template <typename T>
+void add_term(c0ip::AxisArgs<T>& a, const T* in, c0ip::LineOp<T> op, T alpha) {
+  a.in[a.nterms] = in;
+  a.op[a.nterms] = op;
+  a.alpha[a.nterms] = alpha;
+  a.nterms++;
+}
+
+template <typename T>
+void ensure_tmp(Level& L, int d) {
+  Tables<T>& t = tab<T>(L);
+  int need = (d == 2) ? 3 : 6;
+  for (int i = 0; i < need; ++i) t.tmp[i].alloc(L.ndofs);
+}
+
+// y = A x, or r = b - A x if b != nullptr (sum factorisation; Eqs. c0iptensorvp(3D))
+template <typename T>
+void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStream_t st) {
+  const int d = ctx->d, k = ctx->k;
+  const int64_t n = L.n;
+  Tables<T>& t = tab<T>(L);
+  ensure_tmp<T>(L, d);
+  auto Mo = square_op(t.M, k, n), Lo = square_op(t.L, k, n), Bo = square_op(t.B, k, n);
+  const int64_t n2 = (d == 3) ? n : 1;
+  // x-stage: B_x x, L_x x, M_x x
+  {
+    const c0ip::LineOp<T>* ops[3] = {&Bo, &Lo, &Mo};
+    for (int i = 0; i < 3; ++i) {
+      auto a = axis_args<T>(n, n, n2, 0, t.tmp[i].p);
+      add_term(a, x, *ops[i], T(1));
+      launch_axis(ctx, a, st);
+    }
+  }
+  const T sg = b ? T(-1) : T(1);
+  if (d == 2) {
+    // y = M_y (B_x x) + 2 L_y (L_x x) + B_y (M_x x)
+    auto a = axis_args<T>(n, n, 1, 1, y);
+    add_term(a, (const T*)t.tmp[0].p, Mo, sg);
+    add_term(a, (const T*)t.tmp[1].p, Lo, T(2) * sg);
+    add_term(a, (const T*)t.tmp[2].p, Bo, sg);
+    if (b) { a.z = b; a.gamma = T(1); }
+    launch_axis(ctx, a, st);
+    return;
+  }
+  // y-stage: P = M_y B_x + B_y M_x + 2 L_y L_x ; Q = L_y M_x + M_y L_x ; R = M_y M_x
+  {
+    auto a = axis_args<T>(n, n, n, 1, t.tmp[3].p);
+    add_term(a, (const T*)t.tmp[0].p, Mo, T(1));
+    add_term(a, (const T*)t.tmp[2].p, Bo, T(1));
+    add_term(a, (const T*)t.tmp[1].p, Lo, T(2));
+    launch_axis(ctx, a, st);
+    auto q = axis_args<T>(n, n, n, 1, t.tmp[4].p);
+    add_term(q, (const T*)t.tmp[2].p, Lo, T(1));
+    add_term(q, (const T*)t.tmp[1].p, Mo, T(1));
+    launch_axis(ctx, q, st);
+    auto r = axis_args<T>(n, n, n, 1, t.tmp[5].p);
+    add_term(r, (const T*)t.tmp[2].p, Mo, T(1));
+    launch_axis(ctx, r, st);
+  }
+  // z-stage: y = M_z P + 2 L_z Q + B_z R
+  auto a = axis_args<T>(n, n, n, 2, y);
+  add_term(a, (const T*)t.tmp[3].p, Mo, sg);
+  add_term(a, (const T*)t.tmp[4].p, Lo, T(2) * sg);
+  add_term(a, (const T*)t.tmp[5].p, Bo, sg);
+  if (b) { a.z = b; a.gamma = T(1); }
+  launch_axis(ctx, a, st);
+}
+
+template <typename T>
+void apply_op(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStream_t st) {
+  if (ctx->path == C0IP_PATH_AUTO && L.fused &&
+      c0ip::fused_apply<T>(*L.fused, x, b, y, st, &ctx->launches))
+    return;
+  generic_apply<T>(ctx, L, x, b, y, st);
+}
+
+template <typename T>
+void patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, const int32_t* list,
+                 int64_t count, int atomic, cudaStream_t st) {
+  if (count == 0) return;
+  Tables<T>& t = tab<T>(L);
+  c0ip::PatchArgs<T> a{};
+  a.d = ctx->d; a.k = ctx->k; a.np = 2 * ctx->k - 1;
+  a.N = L.N; a.n = L.n;
+  for (int v = 0; v < 4; ++v) { a.S[v] = t.S[v].p; a.lam[v] = t.lam[v].p; }
+  a.r = r; a.x = x; a.omega = omega;
+  a.list = list; a.count = count; a.atomic = atomic;
+  const int nloc = ipow(a.np, a.d);
+  const int block = 256;
+  const int ppb = std::max(1, block / nloc);
+  const size_t smem = 2 * size_t(ppb) * nloc * sizeof(T);
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute(c0ip::patch_fdm_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t blocks = (count + ppb - 1) / ppb;
+  c0ip::patch_fdm_kernel<T><<<(unsigned)blocks, block, smem, st>>>(a);
+  ctx->launches++;
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, bool reverse,
+                 const T* b, T* x, cudaStream_t st) {
+  Tables<T>& t = tab<T>(L);
+  t.sres.alloc(L.ndofs);
+  const int d = ctx->d;
+  for (int s = 0; s < steps; ++s) {
+    if (sm == C0IP_MVS) {
+      const int nc = 1 << (d + 1);
+      for (int ci = 0; ci < nc; ++ci) {
+        int c = reverse ? nc - 1 - ci : ci;
+        int64_t cnt = L.color_off[c + 1] - L.color_off[c];
+        if (cnt == 0) continue;
+        if (ctx->path == C0IP_PATH_AUTO && L.fused &&
+            c0ip::fused_mvs_color<T>(*L.fused, c, omega, b, x, st, &ctx->launches))
+          continue;
+        apply_op<T>(ctx, L, x, b, t.sres.p, st);                 // residual per colour
+        patch_solve<T>(ctx, L, t.sres.p, x, omega, L.colors_d.p + L.color_off[c], cnt, 0, st);
+      }
+      continue;
+    }
+    if (sm == C0IP_AVS_DETERMINISTIC && ctx->path == C0IP_PATH_AUTO && L.fused &&
+        c0ip::fused_avs<T>(*L.fused, omega, b, x, t.sres.p, st, &ctx->launches))
+      continue;
+    apply_op<T>(ctx, L, x, b, t.sres.p, st);                     // one residual per AVS step
+    if (sm == C0IP_AVS_ATOMIC) {
+      patch_solve<T>(ctx, L, t.sres.p, x, omega, nullptr, L.npatch, 1, st);
+    } else {   // coloured / deterministic generic: serialise writes over the 2^d parity classes
+      for (int c = 0; c < (1 << d); ++c) {
+        int64_t cnt = L.parity_off[c + 1] - L.parity_off[c];
+        patch_solve<T>(ctx, L, t.sres.p, x, omega, L.parity_d.p + L.parity_off[c], cnt, 0, st);
+      }
+    }
+  }
+}
+
+// fine += P coarse  (P = E (x) E (x) E, natural embedding)
+template <typename T>
+void prolongate_add_impl(c0ip_ctx ctx, Level& F, const T* coarse, T* fine, cudaStream_t st) {
+  Tables<T>& t = tab<T>(F);
+  ensure_tmp<T>(F, ctx->d);
+  const int64_t nf = F.n, nc = F.E.cols;
+  c0ip::LineOp<T> E;
+  E.v = t.E.p; E.lo = F.Elo.p; E.width = F.E.width; E.hw = 0; E.n_in = nc;
+  if (ctx->d == 2) {
+    auto a = axis_args<T>(nf, nc, 1, 0, t.tmp[0].p);
+    add_term(a, coarse, E, T(1));
+    launch_axis(ctx, a, st);
+    auto b = axis_args<T>(nf, nf, 1, 1, fine);
+    add_term(b, (const T*)t.tmp[0].p, E, T(1));
+    b.beta = T(1);
+    launch_axis(ctx, b, st);
+    return;
+  }
+  auto a = axis_args<T>(nf, nc, nc, 0, t.tmp[0].p);
+  add_term(a, coarse, E, T(1));
+  launch_axis(ctx, a, st);
+  auto b = axis_args<T>(nf, nf, nc, 1, t.tmp[1].p);
+  add_term(b, (const T*)t.tmp[0].p, E, T(1));
+  launch_axis(ctx, b, st);
+  auto c = axis_args<T>(nf, nf, nf, 2, fine);
+  add_term(c, (const T*)t.tmp[1].p, E, T(1));
+  c.beta = T(1);
+  launch_axis(ctx, c, st);
+}
+
+// coarse = P^T fine (restriction = transpose of the embedding)
+template <typename T>
+void restrict_impl(c0ip_ctx ctx, Level& F, const T* fine, T* coarse, cudaStream_t st) {
+  Tables<T>& t = tab<T>(F);
+  ensure_tmp<T>(F, ctx->d);
+  const int64_t nf = F.n, nc = F.E.cols;
+  c0ip::LineOp<T> Et;
+  Et.v = t.Et.p; Et.lo = F.Etlo.p; Et.width = F.Et.width; Et.hw = 0; Et.n_in = nf;
+  if (ctx->d == 2) {
+    auto a = axis_args<T>(nc, nf, 1, 0, t.tmp[0].p);
+    add_term(a, fine, Et, T(1));
+    launch_axis(ctx, a, st);
+    auto b = axis_args<T>(nc, nc, 1, 1, coarse);
+    add_term(b, (const T*)t.tmp[0].p, Et, T(1));
+    launch_axis(ctx, b, st);
+    return;
+  }
+  auto a = axis_args<T>(nc, nf, nf, 0, t.tmp[0].p);
+  add_term(a, fine, Et, T(1));
+  launch_axis(ctx, a, st);
+  auto b = axis_args<T>(nc, nc, nf, 1, t.tmp[1].p);
+  add_term(b, (const T*)t.tmp[0].p, Et, T(1));
+  launch_axis(ctx, b, st);
+  auto c = axis_args<T>(nc, nc, nc, 2, coarse);
+  add_term(c, (const T*)t.tmp[1].p, Et, T(1));
+  launch_axis(ctx, c, st);
+}
+
+template <typename T>
+void fill(c0ip_ctx ctx, T* p, int64_t n, T v, cudaStream_t st) {
+  c0ip::fill_kernel<T><<<grid_for(n), 256, 0, st>>>(n, v, p);
+  ctx->launches++;
+  CK(cudaGetLastError());
+}
+
+template <typename T>
+void axpby(c0ip_ctx ctx, int64_t n, T a, const T* x, T b, T* y, cudaStream_t st) {
+  c0ip::axpby_kernel<T><<<grid_for(n), 256, 0, st>>>(n, a, x, b, y);
+  ctx->launches++;
+  CK(cudaGetLastError());
+}
+
+template <typename Tin, typename Tout>
+void convert(c0ip_ctx ctx, int64_t n, const Tin* x, Tout* y, cudaStream_t st) {
+  c0ip::convert_kernel<Tin, Tout><<<grid_for(n), 256, 0, st>>>(n, x, y);
+  ctx->launches++;
+  CK(cudaGetLastError());
+}
+
+// MG_l(x = 0, b): Algorithm 1; coarsest level: one smoothing step (reading Q12)
+template <typename T>
+void vcycle_rec(c0ip_ctx ctx, int l, const c0ip_mg_config& mg, T* x, const T* b, cudaStream_t st) {
+  Level& L = ctx->levels[l];
+  Tables<T>& t = tab<T>(L);
+  fill<T>(ctx, x, L.ndofs, T(0), st);
+  if (l == ctx->lmin) {
+    smooth_impl<T>(ctx, L, mg.smoother, 1, (T)mg.omega, false, b, x, st);
+    return;
+  }
+  smooth_impl<T>(ctx, L, mg.smoother, mg.steps, (T)mg.omega, false, b, x, st);
+  t.vr.alloc(L.ndofs);
+  apply_op<T>(ctx, L, x, b, t.vr.p, st);                    // r_l = b - A x
+  Level& C = ctx->levels[l - 1];
+  Tables<T>& tc = tab<T>(C);
+  tc.vx.alloc(C.ndofs);
+  tc.vb.alloc(C.ndofs);
+  restrict_impl<T>(ctx, L, t.vr.p, tc.vb.p, st);
+  vcycle_rec<T>(ctx, l - 1, mg, tc.vx.p, tc.vb.p, st);
+  prolongate_add_impl<T>(ctx, L, tc.vx.p, x, st);
+  smooth_impl<T>(ctx, L, mg.smoother, mg.steps, (T)mg.omega,
+                 mg.symmetric && mg.smoother == C0IP_MVS, b, x, st);
+}
+
+void vcycle_top(c0ip_ctx ctx, const c0ip_mg_config& mg, const double* r, double* z, cudaStream_t st) {
+  Level& L = ctx->levels[ctx->lmax];
+  if (mg.cycle_dtype == C0IP_F64) {
+    vcycle_rec<double>(ctx, ctx->lmax, mg, z, r, st);
+  } else {
+    Tables<float>& t = L.t32;
+    t.vx.alloc(L.ndofs);
+    t.vb.alloc(L.ndofs);
+    convert<double, float>(ctx, L.ndofs, r, t.vb.p, st);    // conversion at V-cycle entry
+    vcycle_rec<float>(ctx, ctx->lmax, mg, t.vx.p, t.vb.p, st);
+    convert<float, double>(ctx, L.ndofs, t.vx.p, z, st);
+  }
+}
+
+// dots[i] = <x_i, y_i>, i < nd, read back to host (synchronises the stream)
+void dots(c0ip_ctx ctx, int64_t n, int nd, const double* x0, const double* y0, const double* x1,
+          const double* y1, const double* x2, const double* y2, double* out, cudaStream_t st) {
+  const int G = 296;
+  ctx->dot_part.alloc(3 * G);
+  ctx->dot_out.alloc(3);
+  c0ip::dot_partial_kernel<<<G, 256, 0, st>>>(n, nd, x0, y0, x1 ? x1 : x0, y1 ? y1 : y0,
+                                              x2 ? x2 : x0, y2 ? y2 : y0, ctx->dot_part.p);
+  c0ip::dot_final_kernel<<<1, 256, 0, st>>>(G, ctx->dot_part.p, ctx->dot_out.p);
+  ctx->launches += 2;
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ctx->dot_host, ctx->dot_out.p, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int i = 0; i < nd; ++i) out[i] = ctx->dot_host[i];
+}
+
+c0ip_status check_level(c0ip_ctx ctx, int32_t level) {
+  if (!ctx) return fail(C0IP_ERR_ARG, "null context");
+  if (level < ctx->lmin || level > ctx->lmax)
+    return fail(C0IP_ERR_ARG, "level " + std::to_string(level) + " out of range [" +
+                                  std::to_string(ctx->lmin) + "," + std::to_string(ctx->lmax) + "]");
+  return C0IP_OK;
+}
+
+c0ip_status cuda_fail(const CudaError& e) {
+  if (e.e == cudaErrorMemoryAllocation) return fail(C0IP_ERR_OOM, std::string("out of device memory in ") + e.where);
+  return fail(C0IP_ERR_CUDA, std::string(cudaGetErrorString(e.e)) + " in " + e.where);
+}
+
+#define ABI_TRY try {
+#define ABI_CATCH                                                                  \
+  }                                                                                \
+  catch (const CudaError& e) { return cuda_fail(e); }                              \
+  catch (const std::bad_alloc&) { return fail(C0IP_ERR_OOM, "host allocation failed"); } \
+  catch (const std::exception& e) { return fail(C0IP_ERR_STATE, e.what()); }
+
+void build_level(c0ip_ctx ctx, int l, int64_t N) {
+  Level& L = ctx->levels[l];
+  const int k = ctx->k, d = ctx->d;
+  L.l = l;
+  L.N = N;
+  L.n = k * N - 1;
+  L.h = 1.0 / double(N);
+  L.ndofs = 1;
+  L.npatch = 1;
+  for (int a = 0; a < d; ++a) { L.ndofs *= L.n; L.npatch *= (N - 1); }
+  c0ip::global_bands(ctx->ref, N, L.M, L.L, L.B);
+  const double h = L.h;
+  for (auto& v : L.M.v) v *= h;                       // M = h Mhat
+  for (auto& v : L.L.v) v /= h;                       // L = Lhat / h
+  for (auto& v : L.B.v) v /= h * h * h;               // B = Bhat / h^3
+  if (!c0ip::band_is_spd(L.B))
+    throw std::runtime_error("coercivity: 1D C0IP matrix B is not positive definite (penalty too small)");
+  std::string err;
+  if (!c0ip::make_fdm(ctx->ref, N, L.M, L.L, L.B, L.fdm, err)) throw std::runtime_error("coercivity: " + err);
+  L.t64.M.upload(L.M.v); L.t64.L.upload(L.L.v); L.t64.B.upload(L.B.v);
+  L.t32.M.upload(cast_vec<float>(L.M.v)); L.t32.L.upload(cast_vec<float>(L.L.v)); L.t32.B.upload(cast_vec<float>(L.B.v));
+  for (int v = 0; v < 4; ++v) {
+    if (!L.fdm.present[v]) continue;
+    L.t64.S[v].upload(L.fdm.S[v]); L.t64.lam[v].upload(L.fdm.lam[v]);
+    L.t32.S[v].upload(cast_vec<float>(L.fdm.S[v])); L.t32.lam[v].upload(cast_vec<float>(L.fdm.lam[v]));
+  }
+  // colour and parity-class lists (reading C3)
+  const int nc = 1 << (d + 1), npar = 1 << d;
+  std::vector<std::vector<int32_t>> cl(nc), pl(npar);
+  for (int64_t p = 0; p < L.npatch; ++p) {
+    int64_t v[3] = {0, 0, 0}, q = p;
+    for (int a = 0; a < d; ++a) { v[a] = 1 + q % (N - 1); q /= (N - 1); }
+    int c = color_of(v, d);
+    cl[c].push_back((int32_t)p);
+    pl[c / 2].push_back((int32_t)p);
+  }
+  L.color_off.assign(nc + 1, 0);
+  L.colors_h.clear();
+  for (int c = 0; c < nc; ++c) {
+    L.color_off[c + 1] = L.color_off[c] + (int64_t)cl[c].size();
+    L.colors_h.insert(L.colors_h.end(), cl[c].begin(), cl[c].end());
+  }
+  L.parity_off.assign(npar + 1, 0);
+  L.parity_h.clear();
+  for (int c = 0; c < npar; ++c) {
+    L.parity_off[c + 1] = L.parity_off[c] + (int64_t)pl[c].size();
+    L.parity_h.insert(L.parity_h.end(), pl[c].begin(), pl[c].end());
+  }
+  L.colors_d.upload(L.colors_h);
+  L.parity_d.upload(L.parity_h);
+  L.fused = c0ip::make_fused_level_impl(d, k, N, ctx->ref, L.fdm, h);
+}
+
+void build_transfer(c0ip_ctx ctx, int l) {
+  Level& L = ctx->levels[l];
+  L.E = c0ip::embedding(ctx->k, ctx->levels[l - 1].N);
+  L.Et = c0ip::transpose(L.E);
+  L.t64.E.upload(L.E.v); L.t32.E.upload(cast_vec<float>(L.E.v));
+  L.t64.Et.upload(L.Et.v); L.t32.Et.upload(cast_vec<float>(L.Et.v));
+  L.Elo.upload(L.E.lo);
+  L.Etlo.upload(L.Et.lo);
+}
+
+}  // namespace
+
+// =============================================================================== ABI
+extern "C" {
+
+const char* c0ip_last_error(void) { return g_err.c_str(); }
+
+c0ip_status c0ip_create(const c0ip_config* cfg, c0ip_ctx* out) {
+  if (!cfg || !out) return fail(C0IP_ERR_ARG, "null argument");
+  if (cfg->dim != 2 && cfg->dim != 3) return fail(C0IP_ERR_ARG, "dim must be 2 or 3");
+  if (cfg->degree < 2 || cfg->degree > 7) return fail(C0IP_ERR_ARG, "degree must be in [2,7]");
+  if (cfg->finest_level < 1 || cfg->finest_level > 14) return fail(C0IP_ERR_ARG, "finest_level must be in [1,14]");
+  if (cfg->cells_override < 0 || cfg->cells_override == 1) return fail(C0IP_ERR_ARG, "cells_override must be 0 or >= 2");
+  if (cfg->penalty_scale < 0) return fail(C0IP_ERR_ARG, "penalty_scale must be >= 0");
+  std::unique_ptr<c0ip_ctx_s> ctx(new (std::nothrow) c0ip_ctx_s());
+  if (!ctx) return fail(C0IP_ERR_OOM, "host allocation failed");
+  ABI_TRY
+  CK(cudaSetDevice(cfg->device));
+  ctx->cfg = *cfg;
+  ctx->d = cfg->dim;
+  ctx->k = cfg->degree;
+  const double ps = cfg->penalty_scale > 0 ? cfg->penalty_scale : 1.0;
+  ctx->sigma = ps * ctx->k * (ctx->k + 1);                    // reading Q4
+  ctx->ref = c0ip::make_ref(ctx->k, ctx->sigma);
+  ctx->lmax = cfg->finest_level;
+  ctx->lmin = cfg->cells_override > 0 ? cfg->finest_level : 1;
+  ctx->levels.resize(ctx->lmax + 1);
+  try {
+    for (int l = ctx->lmin; l <= ctx->lmax; ++l)
+      build_level(ctx.get(), l, cfg->cells_override > 0 ? cfg->cells_override : (int64_t(1) << l));
+  } catch (const std::runtime_error& e) {
+    std::string m = e.what();
+    if (m.rfind("coercivity", 0) == 0) return fail(C0IP_ERR_COERCIVITY, m);
+    throw;
+  }
+  for (int l = ctx->lmin + 1; l <= ctx->lmax; ++l) build_transfer(ctx.get(), l);
+  CK(cudaMallocHost(&ctx->dot_host, 4 * sizeof(double)));
+  *out = ctx.release();
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_destroy(c0ip_ctx ctx) {
+  if (!ctx) return fail(C0IP_ERR_ARG, "null context");
+  delete ctx;
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_set_path(c0ip_ctx ctx, c0ip_path path) {
+  if (!ctx) return fail(C0IP_ERR_ARG, "null context");
+  if (path != C0IP_PATH_AUTO && path != C0IP_PATH_GENERIC) return fail(C0IP_ERR_ARG, "bad path");
+  ctx->path = path;
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_level_info(c0ip_ctx ctx, int32_t level, int64_t* n_dofs, int64_t* n_1d,
+                            int64_t* cells, int64_t* n_patches, int32_t* n_colors) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  Level& L = ctx->levels[level];
+  if (n_dofs) *n_dofs = L.ndofs;
+  if (n_1d) *n_1d = L.n;
+  if (cells) *cells = L.N;
+  if (n_patches) *n_patches = L.npatch;
+  if (n_colors) *n_colors = 1 << (ctx->d + 1);
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_patch_dofs(c0ip_ctx ctx, int32_t level, int64_t patch, int64_t* out) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (!out) return fail(C0IP_ERR_ARG, "null output");
+  Level& L = ctx->levels[level];
+  if (patch < 0 || patch >= L.npatch) return fail(C0IP_ERR_ARG, "patch out of range");
+  const int d = ctx->d, k = ctx->k, np = 2 * k - 1;
+  int64_t v[3] = {0, 0, 0}, q = patch;
+  for (int a = 0; a < d; ++a) { v[a] = 1 + q % (L.N - 1); q /= (L.N - 1); }
+  const int nloc = ipow(np, d);
+  for (int l = 0; l < nloc; ++l) {
+    int64_t g = 0, st = 1;
+    int ll = l;
+    for (int a = 0; a < d; ++a) {
+      g += ((v[a] - 1) * k + ll % np) * st;   // 1D range [(v-1)k, (v+1)k-2] (reading C2)
+      ll /= np;
+      st *= L.n;
+    }
+    out[l] = g;
+  }
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_color_patches(c0ip_ctx ctx, int32_t level, int32_t color, int64_t* out,
+                               int64_t cap, int64_t* count) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (color < 0 || color >= (1 << (ctx->d + 1))) return fail(C0IP_ERR_ARG, "colour out of range");
+  Level& L = ctx->levels[level];
+  int64_t cnt = L.color_off[color + 1] - L.color_off[color];
+  if (count) *count = cnt;
+  if (out) {
+    if (cap < cnt) return fail(C0IP_ERR_ARG, "capacity too small");
+    for (int64_t i = 0; i < cnt; ++i) out[i] = L.colors_h[L.color_off[color] + i];
+  }
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_get_fdm(c0ip_ctx ctx, int32_t level, int32_t variant, double* S, double* lambda) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (variant < 0 || variant > 3) return fail(C0IP_ERR_ARG, "variant out of range");
+  Level& L = ctx->levels[level];
+  if (!L.fdm.present[variant]) return fail(C0IP_ERR_STATE, "variant not present on this level");
+  if (S) std::memcpy(S, L.fdm.S[variant].data(), L.fdm.S[variant].size() * sizeof(double));
+  if (lambda) std::memcpy(lambda, L.fdm.lam[variant].data(), L.fdm.lam[variant].size() * sizeof(double));
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_get_matrices_1d(c0ip_ctx ctx, int32_t level, double* M, double* Lm, double* B) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  Level& L = ctx->levels[level];
+  if (L.n > 4096) return fail(C0IP_ERR_ARG, "n_1d too large for a dense export");
+  const int64_t n = L.n;
+  for (int which = 0; which < 3; ++which) {
+    double* dst = which == 0 ? M : (which == 1 ? Lm : B);
+    const c0ip::Band& src = which == 0 ? L.M : (which == 1 ? L.L : L.B);
+    if (!dst) continue;
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < n; ++j) dst[i * n + j] = src.at(i, j);
+  }
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_rhs(c0ip_ctx ctx, int32_t level, double* b, void* stream) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (!b) return fail(C0IP_ERR_ARG, "null output");
+  ABI_TRY
+  Level& L = ctx->levels[level];
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<double> f1 = c0ip::sine_load_1d(ctx->k, L.N);
+  DevArr<double> tmp;
+  tmp.upload(f1);
+  const double c = double(ctx->d * ctx->d) * std::pow(M_PI, 4);   // f = d^2 pi^4 prod sin (Q1, Q8)
+  c0ip::outer_load_kernel<<<grid_for(L.ndofs), 256, 0, st>>>(ctx->d, L.n, tmp.p, c, b);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  tmp.free();
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_apply(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, const void* x, void* y, void* stream) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (!x || !y) return fail(C0IP_ERR_ARG, "null vector");
+  ABI_TRY
+  Level& L = ctx->levels[level];
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dt == C0IP_F64) apply_op<double>(ctx, L, (const double*)x, nullptr, (double*)y, st);
+  else if (dt == C0IP_F32) apply_op<float>(ctx, L, (const float*)x, nullptr, (float*)y, st);
+  else return fail(C0IP_ERR_ARG, "bad dtype");
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_residual(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, const void* b, const void* x,
+                          void* r, void* stream) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (!x || !b || !r) return fail(C0IP_ERR_ARG, "null vector");
+  ABI_TRY
+  Level& L = ctx->levels[level];
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dt == C0IP_F64) apply_op<double>(ctx, L, (const double*)x, (const double*)b, (double*)r, st);
+  else if (dt == C0IP_F32) apply_op<float>(ctx, L, (const float*)x, (const float*)b, (float*)r, st);
+  else return fail(C0IP_ERR_ARG, "bad dtype");
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_smooth(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, c0ip_smoother sm, int32_t steps,
+                        double omega, int32_t reverse_colors, const void* b, void* x, void* stream) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (!x || !b) return fail(C0IP_ERR_ARG, "null vector");
+  if (steps < 0) return fail(C0IP_ERR_ARG, "steps must be >= 0");
+  if (sm < C0IP_AVS_ATOMIC || sm > C0IP_MVS) return fail(C0IP_ERR_ARG, "bad smoother");
+  ABI_TRY
+  Level& L = ctx->levels[level];
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dt == C0IP_F64)
+    smooth_impl<double>(ctx, L, sm, steps, omega, reverse_colors != 0, (const double*)b, (double*)x, st);
+  else if (dt == C0IP_F32)
+    smooth_impl<float>(ctx, L, sm, steps, (float)omega, reverse_colors != 0, (const float*)b, (float*)x, st);
+  else return fail(C0IP_ERR_ARG, "bad dtype");
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_restrict(c0ip_ctx ctx, int32_t fine_level, c0ip_dtype dt, const void* fine, void* coarse,
+                          void* stream) {
+  c0ip_status s = check_level(ctx, fine_level);
+  if (s) return s;
+  if (fine_level <= ctx->lmin) return fail(C0IP_ERR_ARG, "fine_level must be above the coarsest level");
+  if (!fine || !coarse) return fail(C0IP_ERR_ARG, "null vector");
+  ABI_TRY
+  Level& L = ctx->levels[fine_level];
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dt == C0IP_F64) restrict_impl<double>(ctx, L, (const double*)fine, (double*)coarse, st);
+  else if (dt == C0IP_F32) restrict_impl<float>(ctx, L, (const float*)fine, (float*)coarse, st);
+  else return fail(C0IP_ERR_ARG, "bad dtype");
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_prolongate_add(c0ip_ctx ctx, int32_t fine_level, c0ip_dtype dt, const void* coarse,
+                                void* fine, void* stream) {
+  c0ip_status s = check_level(ctx, fine_level);
+  if (s) return s;
+  if (fine_level <= ctx->lmin) return fail(C0IP_ERR_ARG, "fine_level must be above the coarsest level");
+  if (!fine || !coarse) return fail(C0IP_ERR_ARG, "null vector");
+  ABI_TRY
+  Level& L = ctx->levels[fine_level];
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dt == C0IP_F64) prolongate_add_impl<double>(ctx, L, (const double*)coarse, (double*)fine, st);
+  else if (dt == C0IP_F32) prolongate_add_impl<float>(ctx, L, (const float*)coarse, (float*)fine, st);
+  else return fail(C0IP_ERR_ARG, "bad dtype");
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+static c0ip_status check_mg(c0ip_ctx ctx, const c0ip_mg_config* mg) {
+  if (!ctx || !mg) return fail(C0IP_ERR_ARG, "null argument");
+  if (ctx->lmin == ctx->lmax && ctx->cfg.cells_override > 0)
+    return fail(C0IP_ERR_STATE, "multigrid needs the nested hierarchy (cells_override = 0)");
+  if (mg->smoother < C0IP_AVS_ATOMIC || mg->smoother > C0IP_MVS) return fail(C0IP_ERR_ARG, "bad smoother");
+  if (mg->steps < 1) return fail(C0IP_ERR_ARG, "steps must be >= 1");
+  if (mg->cycle_dtype != C0IP_F64 && mg->cycle_dtype != C0IP_F32) return fail(C0IP_ERR_ARG, "bad cycle dtype");
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_vcycle(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* r, double* z, void* stream) {
+  c0ip_status s = check_mg(ctx, mg);
+  if (s) return s;
+  if (!r || !z) return fail(C0IP_ERR_ARG, "null vector");
+  ABI_TRY
+  vcycle_top(ctx, *mg, r, z, (cudaStream_t)stream);
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_pcg(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, double* x, double rtol,
+                     int32_t max_iter, c0ip_report* rep, double* res_history, void* stream) {
+  c0ip_status s = check_mg(ctx, mg);
+  if (s) return s;
+  if (!b || !x) return fail(C0IP_ERR_ARG, "null vector");
+  if (max_iter < 0 || !(rtol >= 0)) return fail(C0IP_ERR_ARG, "bad rtol / max_iter");
+  ABI_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  auto t0 = std::chrono::steady_clock::now();
+  Level& L = ctx->levels[ctx->lmax];
+  const int64_t n = L.ndofs;
+  ctx->pcg_r.alloc(n); ctx->pcg_z.alloc(n); ctx->pcg_p.alloc(n); ctx->pcg_Ap.alloc(n);
+  double *r = ctx->pcg_r.p, *z = ctx->pcg_z.p, *p = ctx->pcg_p.p, *Ap = ctx->pcg_Ap.p;
+  // Saad Alg. 9.1 (textbook PCG), x0 given (reading Q19: callers pass 0)
+  apply_op<double>(ctx, L, x, b, r, st);                          // r = b - A x
+  vcycle_top(ctx, *mg, r, z, st);                                 // z = MG(r)
+  CK(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  double dd[3];
+  dots(ctx, n, 2, r, z, r, r, nullptr, nullptr, dd, st);
+  double rz = dd[0], r0 = std::sqrt(dd[1]), rn = r0;
+  if (res_history) res_history[0] = r0;
+  int it = 0;
+  while (it < max_iter && rn > rtol * r0) {
+    apply_op<double>(ctx, L, p, nullptr, Ap, st);
+    dots(ctx, n, 1, p, Ap, nullptr, nullptr, nullptr, nullptr, dd, st);
+    const double alpha = rz / dd[0];
+    axpby<double>(ctx, n, alpha, p, 1.0, x, st);
+    axpby<double>(ctx, n, -alpha, Ap, 1.0, r, st);
+    ++it;
+    dots(ctx, n, 1, r, r, nullptr, nullptr, nullptr, nullptr, dd, st);
+    rn = std::sqrt(dd[0]);
+    if (res_history) res_history[it] = rn;
+    if (rn <= rtol * r0) break;
+    vcycle_top(ctx, *mg, r, z, st);
+    dots(ctx, n, 1, r, z, nullptr, nullptr, nullptr, nullptr, dd, st);
+    const double beta = dd[0] / rz;
+    rz = dd[0];
+    axpby<double>(ctx, n, 1.0, z, beta, p, st);                   // p = z + beta p
+  }
+  CK(cudaStreamSynchronize(st));
+  auto t1 = std::chrono::steady_clock::now();
+  if (rep) {
+    rep->iterations = it;
+    rep->converged = (rn <= rtol * r0) ? 1 : 0;
+    rep->r0 = r0;
+    rep->rn = rn;
+    double ratio = (r0 > 0) ? rn / r0 : 0.0;
+    rep->nu = (it == 0 || ratio <= 0) ? 0.0 : -8.0 / std::log10(std::pow(ratio, 1.0 / it));
+    rep->seconds = std::chrono::duration<double>(t1 - t0).count();
+  }
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_launch_count(c0ip_ctx ctx, int64_t* count) {
+  if (!ctx || !count) return fail(C0IP_ERR_ARG, "null argument");
+  *count = ctx->launches;
+  return C0IP_OK;
+}
+
+}  // extern "C"

