@@ -1,18 +1,24 @@
 // Fused tile kernels for large 2D levels (sm_100a, FP64 and FP32).
 //
 // Two kernels make one additive smoothing step:
-//   apply2d  : r = b - A x  (or y = A x) for a tile of C x C cells, all 1D contractions of the
-//              Kronecker sum A = h^-2 (M^_y B^_x + 2 L^_y L^_x + B^_y M^_x) done
-//              in shared memory on a halo'd box of x;
-//   fdm2d    : x += omega h^2 sum_v R_v^T A^~_v^{-1} R_v r for the same tile,
+//   apply2d  : r = b - A x  (or y = A x) for a tile of C x C cells; all 1D contractions of the
+//              Kronecker sum A = h^-2 (M^_y B^_x + 2 L^_y L^_x + B^_y M^_x) in
+//              shared memory on a halo'd box of x;
+//   fdm2d    : x += omega h^2 sum_v R_v^T A~_v^{-1} R_v r for the same tile,
 //              written as a GATHER: the patch-eigenbasis transform S^T R_v is shared by all
 //              patches of a patch row, every owned DoF sums its <= 4 patch corrections in a
-//              fixed order (deterministic, no atomics), and the result is stored once.
-// Work is organised so that every lane of a warp applies the *same* coefficients (same class
-// p = j mod k of the output node, or same patch axis variant): the coefficients live in the
-// kernel parameter bank (__grid_constant__) and feed DFMA/FFMA as constant-bank operands.
-// Tiles touching the domain boundary take a uniform per-warp branch to the one-sided face rows
-// and the left/right patch variants.
+//              fixed order (deterministic, no atomics) and is stored once.
+// Both kernels are persistent: each CTA walks tiles t, t + gridDim.x, ... and prefetches the
+// next tile's inputs with cp.async while computing the current one.
+//
+// Coefficients.  Every lane of a warp applies the *same* coefficients (same class p = j mod k of
+// the output node, or same patch axis variant), so they are read from the kernel parameter bank
+// (__grid_constant__) as uniform-register operands of DFMA/FFMA (LDCU + DFMA R, R, UR, R).  Each
+// loaded coefficient is reused for RB independent lines held by the same thread (register
+// blocking), and the coefficient base is offset by an opaque zero per round so that the compiler
+// issues the LDCU at the point of use instead of hoisting hundreds of constants into registers.
+// Tiles touching the domain boundary take a uniform per-warp branch to the one-sided face rows and
+// the left/right patch variants.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,9 +27,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
-#include <vector>
-
 #include <type_traits>
+#include <vector>
 
 #include "fused_dispatch.hpp"
 
@@ -51,6 +56,7 @@ struct ApplyP {
   T* y;
   int64_t N, n;             // cells, 1D interior dofs (n = KN-1)
   T scale;                  // h^-2
+  int zero;                 // 0 at run time (opaque to the compiler)
 };
 
 template <typename T, int K>
@@ -60,6 +66,7 @@ struct FdmP {
   T* x;
   int64_t N, n;
   T factor;                 // omega * h^2
+  int zero;
 };
 
 template <int K>
@@ -69,56 +76,21 @@ struct Tile {
   static constexpr int O = C * K;
 };
 
+template <typename T, int K>
+struct Blk {
+  // register blocking factor (lines per thread sharing one coefficient load)
+  static constexpr int RB = (sizeof(T) == 8) ? (K <= 5 ? 2 : 1) : 2;
+};
+
 __host__ __device__ constexpr int odd(int v) { return v | 1; }
+__host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
 
-// ----------------------------------------------------------------------------- banded rows
-// B row of an output node of class P (j = cK + P): w[0] <-> node (c-2)K, columns j-2K..j+2K.
-// Structural zeros (column outside the support of row P) are skipped at compile time.
-template <typename T, int K, int P, typename F>
-__device__ __forceinline__ T rowB(F coef, const T* w) {
-  T s = 0;
-#pragma unroll
-  for (int q = 0; q <= 4 * K; ++q)
-    if (P == 0 || (q >= K - P && q <= 4 * K - P)) s = fma(coef(q), w[P + q], s);
-  return s;
-}
-// M or L row (bandwidth K): w2[0] <-> node (c-1)K, coefficient index q <-> column j - K + q.
-template <typename T, int K, int P, typename F>
-__device__ __forceinline__ T rowML(F coef, const T* w2) {
-  T s = 0;
-#pragma unroll
-  for (int q = 0; q <= 2 * K; ++q)
-    if (P == 0 || (q >= K - P && q <= 2 * K - P)) s = fma(coef(q), w2[P + q], s);
-  return s;
+template <typename T, int K>
+__device__ __forceinline__ const Coef2<T, K>& coef_at(const Coef2<T, K>& c, int off) {
+  return *reinterpret_cast<const Coef2<T, K>*>(reinterpret_cast<const char*>(&c) + off);
 }
 
-// x-stage of one output node: (B^ x, L^ x, M^ x) for class P, interior (s < 0) or special row s
-template <typename T, int K, int P>
-__device__ __forceinline__ void stage_x_node(const Coef2<T, K>& c, int s, const T* w, T& b, T& l, T& m) {
-  if (s < 0) {
-    b = rowB<T, K, P>([&](int q) { return c.BI[P][q]; }, w);
-    l = rowML<T, K, P>([&](int q) { return c.LI[P][q]; }, w + K);
-    m = rowML<T, K, P>([&](int q) { return c.MI[P][q]; }, w + K);
-  } else {
-    b = rowB<T, K, P>([&](int q) { return c.BS[s][q]; }, w);
-    l = rowML<T, K, P>([&](int q) { return c.LS[s][q + K]; }, w + K);
-    m = rowML<T, K, P>([&](int q) { return c.MS[s][q + K]; }, w + K);
-  }
-}
-
-// y-stage of one output node: B^(wM) + M^(wB) + 2 L^(wL)   (wB2/wL2: base (c-1)K)
-template <typename T, int K, int P>
-__device__ __forceinline__ T stage_y_node(const Coef2<T, K>& c, int s, const T* wM, const T* wB2, const T* wL2) {
-  if (s < 0)
-    return rowB<T, K, P>([&](int q) { return c.BI[P][q]; }, wM) +
-           rowML<T, K, P>([&](int q) { return c.MI[P][q]; }, wB2) +
-           T(2) * rowML<T, K, P>([&](int q) { return c.LI[P][q]; }, wL2);
-  return rowB<T, K, P>([&](int q) { return c.BS[s][q]; }, wM) +
-         rowML<T, K, P>([&](int q) { return c.MS[s][q + K]; }, wB2) +
-         T(2) * rowML<T, K, P>([&](int q) { return c.LS[s][q + K]; }, wL2);
-}
-
-// compile-time dispatch of a runtime-unrolled class index p (p is a constant after unrolling)
+// compile-time dispatch of an unrolled index p (p is a constant after unrolling)
 template <int K, typename F>
 __device__ __forceinline__ void with_p(int p, F f) {
   switch (p) {
@@ -140,268 +112,526 @@ __device__ __forceinline__ int special_row(int64_t j, int64_t N) {
   return -1;
 }
 
+__device__ __forceinline__ int variant_of(int64_t v, int64_t N) { return v == 1 ? 0 : (v == N - 1 ? 2 : 1); }
+
+// ----------------------------------------------------------------------------- banded rows (RB lines)
+// B row of an output node of class P (j = cK + P): w[r][0] <-> node (c-2)K; columns j-2K..j+2K.
+// acc[r] += sum_q coef(q) w[r][P+q]; structural zeros skipped at compile time.
+template <typename T, int K, int P, int RB, int W, typename F>
+__device__ __forceinline__ void rowB(F coef, const T (&w)[RB][W], int wofs, T (&acc)[RB]) {
+#pragma unroll
+  for (int q = 0; q <= 4 * K; ++q) {
+    if (P == 0 || (q >= K - P && q <= 4 * K - P)) {
+      const T cq = coef(q);
+#pragma unroll
+      for (int r = 0; r < RB; ++r) acc[r] = fma(cq, w[r][wofs + P + q], acc[r]);
+    }
+  }
+}
+// M or L row (bandwidth K): w[r][wofs] <-> node (c-1)K; coefficient q <-> column j - K + q.
+template <typename T, int K, int P, int RB, int W, typename F>
+__device__ __forceinline__ void rowML(F coef, const T (&w)[RB][W], int wofs, T (&acc)[RB]) {
+#pragma unroll
+  for (int q = 0; q <= 2 * K; ++q) {
+    if (P == 0 || (q >= K - P && q <= 2 * K - P)) {
+      const T cq = coef(q);
+#pragma unroll
+      for (int r = 0; r < RB; ++r) acc[r] = fma(cq, w[r][wofs + P + q], acc[r]);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------- async copies
+// cp.async (LDGSTS) element copies global -> shared with zero fill (src-size 0) for the nodes
+// outside the interior (the eliminated clamped-boundary nodes).
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? (int)sizeof(T) : 0;
+  if constexpr (sizeof(T) == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// ROWS x COLS box of nodes starting at node (Y0, X0) into smem with row pitch PITCH
+template <typename T, int ROWS, int COLS, int PITCH>
+__device__ __forceinline__ void load_box_async(T* dst, const T* src, int64_t n, int64_t KN, int64_t Y0,
+                                               int64_t X0) {
+  const bool inner = (X0 >= 1 && X0 + COLS - 1 <= KN - 1 && Y0 >= 1 && Y0 + ROWS - 1 <= KN - 1);
+  const T* base = src + (Y0 - 1) * n + (X0 - 1);
+  if (inner) {
+    for (int e = threadIdx.x; e < ROWS * COLS; e += blockDim.x) {
+      const int r = e / COLS, c = e - (e / COLS) * COLS;
+      cp_async_elem(dst + r * PITCH + c, base + (int64_t)r * n + c, true);
+    }
+  } else {
+    for (int e = threadIdx.x; e < ROWS * COLS; e += blockDim.x) {
+      const int r = e / COLS, c = e - (e / COLS) * COLS;
+      const int64_t jy = Y0 + r, jx = X0 + c;
+      const bool ok = (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1);
+      cp_async_elem(dst + r * PITCH + c, ok ? base + (int64_t)r * n + c : src, ok);
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------- apply2d
 template <typename T, int K>
-__global__ void __launch_bounds__(256) apply2d_kernel(const __grid_constant__ ApplyP<T, K> P) {
-  constexpr int C = Tile<K>::C, O = Tile<K>::O;
-  constexpr int BW = (C + 3) * K + 1;       // box: nodes [(c0-2)K, (c0+C+1)K]
-  constexpr int PX = odd(BW), PO = odd(O);
+struct ApplyLayout {
+  static constexpr int C = Tile<K>::C, O = Tile<K>::O, RB = Blk<T, K>::RB;
+  static constexpr int BW = (C + 3) * K + 1;       // box: nodes [(c0-2)K, (c0+C+1)K]
+  static constexpr int PX = odd(BW), PO = odd(O);
+  static constexpr int XB = BW * PX, BB = O * PO;  // box, b tile
+  static constexpr int STAGE = BW * PO;            // one of the three x-stage outputs
+  static constexpr int TOTAL = 2 * (XB + BB) + 3 * STAGE;
+  static constexpr int GX = cdiv(BW, RB);          // row groups of the x-stage
+  static constexpr int GY = cdiv(O, RB);           // column groups of the y-stage
+};
+
+template <typename T, int K>
+__global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__ ApplyP<T, K> P) {
+  using LY = ApplyLayout<T, K>;
+  constexpr int C = LY::C, O = LY::O, BW = LY::BW, PX = LY::PX, PO = LY::PO, RB = LY::RB;
+  constexpr int GX = LY::GX, GY = LY::GY;
+  constexpr int NT = 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* xb = reinterpret_cast<T*>(smem_raw);
-  T* sB = xb + BW * PX;
-  T* sL = sB + BW * PO;
-  T* sM = sL + BW * PO;
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  T* const xbuf0 = sm;                           // [2][XB]
+  T* const bbuf0 = sm + 2 * LY::XB;              // [2][BB]
+  T* sB = sm + 2 * (LY::XB + LY::BB);
+  T* sL = sB + LY::STAGE;
+  T* sM = sL + LY::STAGE;
   const int64_t N = P.N, n = P.n, KN = K * N;
-  const int64_t cx0 = (int64_t)blockIdx.x * C, cy0 = (int64_t)blockIdx.y * C;
-  const int64_t X0 = (cx0 - 2) * K, Y0 = (cy0 - 2) * K;
+  const int ntx = int((N + C - 1) / C);
+  const int ntiles = ntx * ntx;
   const int tid = threadIdx.x;
 
-  for (int e = tid; e < BW * BW; e += blockDim.x) {
-    const int r = e / BW, cc = e % BW;
-    const int64_t jy = Y0 + r, jx = X0 + cc;
-    T v = 0;
-    if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1) v = P.x[(jy - 1) * n + (jx - 1)];
-    xb[r * PX + cc] = v;
-  }
-  __syncthreads();
+  auto issue = [&](int t, int buf) {
+    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(t / ntx) * C;
+    load_box_async<T, BW, BW, PX>(xbuf0 + buf * LY::XB, P.x, n, KN, (cy0 - 2) * K, (cx0 - 2) * K);
+    if (P.b) load_box_async<T, O, O, PO>(bbuf0 + buf * LY::BB, P.b, n, KN, cy0 * K, cx0 * K);
+  };
 
-  // x-stage: B^_x x, L^_x x, M^_x x on all box rows, owned columns.  lanes <-> rows.
-  for (int u = tid; u < BW * C; u += blockDim.x) {
-    const int r = u % BW, ci = u / BW;
-    const int64_t cx = cx0 + ci;
-    if (cx >= N) continue;
-    T w[4 * K + 1];
-#pragma unroll
-    for (int q = 0; q <= 4 * K; ++q) w[q] = xb[r * PX + ci * K + q];
-    T ob[K], ol[K], om[K];
-    const bool inner = (cx >= 2 && cx <= N - 2);
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const int s = inner ? -1 : special_row<K>(cx * K + p, N);
-      with_p<K>(p, [&](auto PC) {
-        constexpr int PP = decltype(PC)::value;
-        stage_x_node<T, K, PP>(P.c, s, w, ob[PP], ol[PP], om[PP]);
-      });
-    }
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      sB[r * PO + ci * K + p] = ob[p];
-      sL[r * PO + ci * K + p] = ol[p];
-      sM[r * PO + ci * K + p] = om[p];
-    }
-  }
-  __syncthreads();
+  int buf = 0, round = 0;
+  if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  cp_async_commit();
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (t + (int)gridDim.x < ntiles) issue(t + gridDim.x, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    const T* xb = xbuf0 + buf * LY::XB;
+    const T* bt = bbuf0 + buf * LY::BB;
+    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(t / ntx) * C;
 
-  // y-stage: y = h^-2 (M^_y (B^_x x) + 2 L^_y (L^_x x) + B^_y (M^_x x)).  lanes <-> columns.
-  for (int u = tid; u < O * C; u += blockDim.x) {
-    const int col = u % O, ci = u / O;
-    const int64_t cy = cy0 + ci;
-    const int64_t jx = cx0 * K + col;
-    if (cy >= N || jx < 1 || jx > KN - 1) continue;
-    T wM[4 * K + 1], wB[2 * K + 1], wL[2 * K + 1];
+    // x-stage: B^_x x, L^_x x, M^_x x on all box rows, owned columns.  lanes <-> row groups;
+    // a thread holds rows g, g + GX, ... (RB rows) of one cell and reuses every coefficient RB times.
+#pragma unroll 1
+    for (int it = 0; it < cdiv(GX * C, NT); ++it, ++round) {
+      const int u = it * NT + tid;
+      if (u >= GX * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      const int g = u % GX, ci = u / GX;
+      const int64_t cx = cx0 + ci;
+      if (cx >= N) continue;
+      T w[RB][4 * K + 1];
 #pragma unroll
-    for (int q = 0; q <= 4 * K; ++q) wM[q] = sM[(ci * K + q) * PO + col];
+      for (int r = 0; r < RB; ++r) {
+        const int row = min(g + r * GX, BW - 1);
 #pragma unroll
-    for (int q = 0; q <= 2 * K; ++q) {
-      wB[q] = sB[(ci * K + K + q) * PO + col];
-      wL[q] = sL[(ci * K + K + q) * PO + col];
+        for (int q = 0; q <= 4 * K; ++q) w[r][q] = xb[row * PX + ci * K + q];
+      }
+      const bool inner = (cx >= 2 && cx <= N - 2);
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        T ob[RB], ol[RB], om[RB];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) ob[r] = ol[r] = om[r] = 0;
+        const int s = inner ? -1 : special_row<K>(cx * K + p, N);
+        with_p<K>(p, [&](auto PC) {
+          constexpr int PP = decltype(PC)::value;
+          if (s < 0) {
+            rowB<T, K, PP>([&](int q) { return c.BI[PP][q]; }, w, 0, ob);
+            rowML<T, K, PP>([&](int q) { return c.LI[PP][q]; }, w, K, ol);
+            rowML<T, K, PP>([&](int q) { return c.MI[PP][q]; }, w, K, om);
+          } else {
+            rowB<T, K, PP>([&](int q) { return c.BS[s][q]; }, w, 0, ob);
+            rowML<T, K, PP>([&](int q) { return c.LS[s][q + K]; }, w, K, ol);
+            rowML<T, K, PP>([&](int q) { return c.MS[s][q + K]; }, w, K, om);
+          }
+        });
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const int row = g + r * GX;
+          if (row < BW) {
+            sB[row * PO + ci * K + p] = ob[r];
+            sL[row * PO + ci * K + p] = ol[r];
+            sM[row * PO + ci * K + p] = om[r];
+          }
+        }
+      }
     }
-    const bool inner = (cy >= 2 && cy <= N - 2);
+    __syncthreads();
+
+    // y-stage: y = h^-2 (B^_y (M^_x x) + M^_y (B^_x x) + 2 L^_y (L^_x x)).  lanes <-> column
+    // groups; three passes (one window at a time) accumulate K outputs for RB columns.
+#pragma unroll 1
+    for (int it = 0; it < cdiv(GY * C, NT); ++it, ++round) {
+      const int u = it * NT + tid;
+      if (u >= GY * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      const int g = u % GY, ci = u / GY;
+      const int64_t cy = cy0 + ci;
+      if (cy >= N) continue;
+      const bool inner = (cy >= 2 && cy <= N - 2);
+      T acc[K][RB];
 #pragma unroll
-    for (int p = 0; p < K; ++p) {
-      const int64_t j = cy * K + p;
-      if (j < 1 || j > KN - 1) continue;
-      const int s = inner ? -1 : special_row<K>(j, N);
-      T v = 0;
-      with_p<K>(p, [&](auto PC) {
-        constexpr int PP = decltype(PC)::value;
-        v = stage_y_node<T, K, PP>(P.c, s, wM, wB, wL);
-      });
-      const int64_t g = (j - 1) * n + (jx - 1);
-      v *= P.scale;
-      P.y[g] = P.b ? P.b[g] - v : v;
+      for (int p = 0; p < K; ++p)
+#pragma unroll
+        for (int r = 0; r < RB; ++r) acc[p][r] = 0;
+      int col[RB];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) col[r] = min(g + r * GY, O - 1);
+      {
+        T w[RB][4 * K + 1];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int q = 0; q <= 4 * K; ++q) w[r][q] = sM[(ci * K + q) * PO + col[r]];
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const int s = inner ? -1 : special_row<K>(cy * K + p, N);
+          with_p<K>(p, [&](auto PC) {
+            constexpr int PP = decltype(PC)::value;
+            if (s < 0) rowB<T, K, PP>([&](int q) { return c.BI[PP][q]; }, w, 0, acc[PP]);
+            else rowB<T, K, PP>([&](int q) { return c.BS[s][q]; }, w, 0, acc[PP]);
+          });
+        }
+      }
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass) {
+        const T* src = pass == 0 ? sB : sL;
+        T w[RB][2 * K + 1];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int q = 0; q <= 2 * K; ++q) w[r][q] = src[(ci * K + K + q) * PO + col[r]];
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const int s = inner ? -1 : special_row<K>(cy * K + p, N);
+          T tmp[RB];
+#pragma unroll
+          for (int r = 0; r < RB; ++r) tmp[r] = 0;
+          with_p<K>(p, [&](auto PC) {
+            constexpr int PP = decltype(PC)::value;
+            if (pass == 0) {
+              if (s < 0) rowML<T, K, PP>([&](int q) { return c.MI[PP][q]; }, w, 0, tmp);
+              else rowML<T, K, PP>([&](int q) { return c.MS[s][q + K]; }, w, 0, tmp);
+            } else {
+              if (s < 0) rowML<T, K, PP>([&](int q) { return c.LI[PP][q]; }, w, 0, tmp);
+              else rowML<T, K, PP>([&](int q) { return c.LS[s][q + K]; }, w, 0, tmp);
+            }
+          });
+#pragma unroll
+          for (int r = 0; r < RB; ++r) acc[p][r] += (pass == 0 ? T(1) : T(2)) * tmp[r];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int cc = g + r * GY;
+        const int64_t jx = cx0 * K + cc;
+        if (cc >= O || jx < 1 || jx > KN - 1) continue;
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const int64_t j = cy * K + p;
+          if (j < 1 || j > KN - 1) continue;
+          const T v = P.scale * acc[p][r];
+          P.y[(j - 1) * n + (jx - 1)] = P.b ? bt[(ci * K + p) * PO + cc] - v : v;
+        }
+      }
     }
+    __syncthreads();
+    buf ^= 1;
   }
 }
 
 // ----------------------------------------------------------------------------- fdm2d
-__device__ __forceinline__ int variant_of(int64_t v, int64_t N) { return v == 1 ? 0 : (v == N - 1 ? 2 : 1); }
-
-// z[i] = sum_l S[l][i] w[l]   (S^T w)
-template <typename T, int K, int V>
-__device__ __forceinline__ void s_t(const Coef2<T, K>& c, const T* w, T* z) {
+// z[r][i] = sum_l S[l][i] w[r][l]   (S^T w) for RB lines
+template <typename T, int K, int V, int RB>
+__device__ __forceinline__ void s_t(const Coef2<T, K>& c, const T (&w)[RB][2 * K - 1], T (&z)[RB][2 * K - 1]) {
   constexpr int NP = 2 * K - 1;
 #pragma unroll
   for (int i = 0; i < NP; ++i) {
-    T s = 0;
 #pragma unroll
-    for (int l = 0; l < NP; ++l) s = fma(c.S[V][l * NP + i], w[l], s);
-    z[i] = s;
+    for (int r = 0; r < RB; ++r) z[r][i] = 0;
+#pragma unroll
+    for (int l = 0; l < NP; ++l) {
+      const T s = c.S[V][l * NP + i];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) z[r][i] = fma(s, w[r][l], z[r][i]);
+    }
   }
 }
 
-// acc[l] += sum_i S[l][i] z[i]   (S z)
-template <typename T, int K, int V>
-__device__ __forceinline__ void s_n(const Coef2<T, K>& c, const T* z, T* acc) {
+// out[r][p] += sum_i S[OFF + p][i] z[r][i] for p in [P0, K)
+template <typename T, int K, int V, int OFF, int P0, int RB>
+__device__ __forceinline__ void s_rows(const Coef2<T, K>& c, const T (&z)[RB][2 * K - 1], T (&out)[RB][K]) {
   constexpr int NP = 2 * K - 1;
 #pragma unroll
-  for (int l = 0; l < NP; ++l) {
-    T s = acc[l];
+  for (int p = P0; p < K; ++p)
 #pragma unroll
-    for (int i = 0; i < NP; ++i) s = fma(c.S[V][l * NP + i], z[i], s);
-    acc[l] = s;
-  }
+    for (int i = 0; i < NP; ++i) {
+      const T s = c.S[V][(OFF + p) * NP + i];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) out[r][p] = fma(s, z[r][i], out[r][p]);
+    }
 }
 
-// out[p] += sum_i S[OFF + p][i] z[i] for p in [P0, K)  (rows OFF+p of patch-local index)
-template <typename T, int K, int V, int OFF, int P0>
-__device__ __forceinline__ void s_rows(const Coef2<T, K>& c, const T* z, T* out) {
-  constexpr int NP = 2 * K - 1;
+template <typename T, int K, int V, int RB>
+__device__ __forceinline__ void s_t_var(int var, const Coef2<T, K>& c, const T (&w)[RB][2 * K - 1],
+                                        T (&z)[RB][2 * K - 1]) {
+  if (var == 1) s_t<T, K, 1, RB>(c, w, z);
+  else if (var == 0) s_t<T, K, 0, RB>(c, w, z);
+  else s_t<T, K, 2, RB>(c, w, z);
+}
+
+// out[r][p] (p < K) for the K nodes of cell `cell`: patch cell (local K-1+p), patch cell+1 (local p-1)
+template <typename T, int K, int RB>
+__device__ __forceinline__ void cell_from_patches(const Coef2<T, K>& c, int64_t cell, int64_t N,
+                                                  const T (&z0)[RB][2 * K - 1], const T (&z1)[RB][2 * K - 1],
+                                                  T (&out)[RB][K]) {
 #pragma unroll
-  for (int p = P0; p < K; ++p) {
-    T s = out[p];
+  for (int r = 0; r < RB; ++r)
 #pragma unroll
-    for (int i = 0; i < NP; ++i) s = fma(c.S[V][(OFF + p) * NP + i], z[i], s);
-    out[p] = s;
+    for (int p = 0; p < K; ++p) out[r][p] = 0;
+  if (cell >= 1 && cell <= N - 1) {
+    const int v0 = variant_of(cell, N);
+    if (v0 == 1) s_rows<T, K, 1, K - 1, 0, RB>(c, z0, out);
+    else if (v0 == 0) s_rows<T, K, 0, K - 1, 0, RB>(c, z0, out);
+    else s_rows<T, K, 2, K - 1, 0, RB>(c, z0, out);
+  }
+  if (cell + 1 >= 1 && cell + 1 <= N - 1) {
+    const int v1 = variant_of(cell + 1, N);
+    if (v1 == 1) s_rows<T, K, 1, -1, 1, RB>(c, z1, out);
+    else if (v1 == 0) s_rows<T, K, 0, -1, 1, RB>(c, z1, out);
+    else s_rows<T, K, 2, -1, 1, RB>(c, z1, out);
   }
 }
 
 template <typename T, int K>
-__global__ void __launch_bounds__(256) fdm2d_kernel(const __grid_constant__ FdmP<T, K> P) {
-  constexpr int C = Tile<K>::C, O = Tile<K>::O, NP = 2 * K - 1;
-  constexpr int RN = (C + 2) * K - 1;          // residual box: nodes [(c0-1)K+1, (c0+C+1)K-1]
-  constexpr int E = (C + 1) * NP;              // patch-eigen columns: patches c0 .. c0+C
-  constexpr int PR = odd(RN), PE = odd(E), PS = odd(O);
+struct FdmLayout {
+  static constexpr int C = Tile<K>::C, O = Tile<K>::O, NP = 2 * K - 1, RB = Blk<T, K>::RB;
+  static constexpr int RN = (C + 2) * K - 1;       // residual box: nodes [(c0-1)K+1, (c0+C+1)K-1]
+  static constexpr int E = (C + 1) * NP;           // patch-eigen columns: patches c0 .. c0+C
+  static constexpr int PR = odd(RN), PE = odd(E), PS = odd(O);
+  static constexpr int RB_ = RN * PR, XT = O * PS; // r box, x tile (prefetched, double buffered)
+  static constexpr int Z1 = RN * PE;               // Z1 [RN][E]; later Z3 [O][E]
+  static constexpr int Z2 = (C + 1) * NP * PE;     // Z2 [vy][iy][E]; later out staging [O][PS]
+  static constexpr int TOTAL = 2 * (RB_ + XT) + Z1 + Z2 + NP * NP;
+  static constexpr int GR = cdiv(RN, RB);          // FX row groups
+  static constexpr int GE = cdiv(E, RB);           // FYg / FYs column groups
+  static constexpr int GO = cdiv(O, RB);           // FS row groups
+};
+
+// x += omega h^2 sum_v R_v^T A~_v^{-1} R_v r on the tile (gather form, see file header):
+//   FX  (row, vx)  Z1[y][vx,i]    = sum_l S_vx[l][i] r[y][(vx-1)K+1+l]
+//   FYg (col, vy)  Z2[vy][i][col] = (sum_l S_vy[l][i] Z1[(vy-1)K+1+l][col]) / (lam_vy,i + lam_vx,ix)
+//   FYs (col, cy)  Z3[y][col]     = sum over the <= 2 patches of row y of S_vy[y-..][i] Z2[vy][i][col]
+//   FS  (row, cx)  out[y][x]      = sum over the <= 2 patches of column x of S_vx[x-..][i] Z3[y][vx,i]
+template <typename T, int K>
+__global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ FdmP<T, K> P) {
+  using LY = FdmLayout<T, K>;
+  constexpr int C = LY::C, O = LY::O, NP = LY::NP, RN = LY::RN, E = LY::E, RB = LY::RB;
+  constexpr int PR = LY::PR, PE = LY::PE, PS = LY::PS, GR = LY::GR, GE = LY::GE, GO = LY::GO;
+  constexpr int NT = 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* rb = reinterpret_cast<T*>(smem_raw);      // [RN][PR]   (later: out staging [O][PS])
-  T* z1 = rb + RN * PR;                        // [RN][PE]
-  T* z3 = z1 + RN * PE;                        // [O][PE]
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  T* const rbuf0 = sm;                           // [2][RB_]
+  T* const xbuf0 = sm + 2 * LY::RB_;             // [2][XT]
+  T* z1 = sm + 2 * (LY::RB_ + LY::XT);
+  T* z3 = z1;                                    // Z1 is dead after FYg
+  T* z2 = z1 + LY::Z1;
+  T* outs = z2;                                  // Z2 is dead after FYs
+  T* invd = z2 + LY::Z2;                         // 1/(lam_int[i] + lam_int[j])
+  static_assert(RN >= O && LY::Z2 >= O * PS, "Z3 / staging do not fit");
   const int64_t N = P.N, n = P.n, KN = K * N;
-  const int64_t cx0 = (int64_t)blockIdx.x * C, cy0 = (int64_t)blockIdx.y * C;
-  const int64_t X0 = (cx0 - 1) * K + 1, Y0 = (cy0 - 1) * K + 1;
+  const int ntx = int((N + C - 1) / C);
+  const int ntiles = ntx * ntx;
   const int tid = threadIdx.x;
 
-  for (int e = tid; e < RN * RN; e += blockDim.x) {
-    const int r = e / RN, cc = e % RN;
-    const int64_t jy = Y0 + r, jx = X0 + cc;
-    T v = 0;
-    if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1) v = P.r[(jy - 1) * n + (jx - 1)];
-    rb[r * PR + cc] = v;
-  }
-  __syncthreads();
+  for (int e = tid; e < NP * NP; e += blockDim.x)
+    invd[e] = T(1) / (P.c.lam[1][e / NP] + P.c.lam[1][e % NP]);
 
-  // FX: Z1[y][v_x, i] = sum_l S_vx[l][i] r[y][(vx-1)K+1+l]   lanes <-> rows, same patch
-  for (int u = tid; u < RN * (C + 1); u += blockDim.x) {
-    const int r = u % RN, pi = u / RN;
-    const int64_t vx = cx0 + pi;
-    T z[NP];
-    if (vx >= 1 && vx <= N - 1) {
-      T w[NP];
+  auto issue = [&](int t, int buf) {
+    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(t / ntx) * C;
+    load_box_async<T, RN, RN, PR>(rbuf0 + buf * LY::RB_, P.r, n, KN, (cy0 - 1) * K + 1, (cx0 - 1) * K + 1);
+    load_box_async<T, O, O, PS>(xbuf0 + buf * LY::XT, P.x, n, KN, cy0 * K, cx0 * K);
+  };
+
+  int buf = 0, round = 0;
+  if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  cp_async_commit();
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (t + (int)gridDim.x < ntiles) issue(t + gridDim.x, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    const T* rb = rbuf0 + buf * LY::RB_;
+    const T* xt = xbuf0 + buf * LY::XT;
+    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(t / ntx) * C;
+
+    // FX: lanes <-> row groups, one patch vx per unit (uniform variant)
+#pragma unroll 1
+    for (int it = 0; it < cdiv(GR * (C + 1), NT); ++it, ++round) {
+      const int u = it * NT + tid;
+      if (u >= GR * (C + 1)) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      const int g = u % GR, pi = u / GR;
+      const int64_t vx = cx0 + pi;
+      T z[RB][NP];
+      if (vx >= 1 && vx <= N - 1) {
+        T w[RB][NP];
 #pragma unroll
-      for (int l = 0; l < NP; ++l) w[l] = rb[r * PR + pi * K + l];
-      const int var = variant_of(vx, N);
-      if (var == 1) s_t<T, K, 1>(P.c, w, z);
-      else if (var == 0) s_t<T, K, 0>(P.c, w, z);
-      else s_t<T, K, 2>(P.c, w, z);
-    } else {
+        for (int r = 0; r < RB; ++r) {
+          const int row = min(g + r * GR, RN - 1);
 #pragma unroll
-      for (int i = 0; i < NP; ++i) z[i] = 0;
+          for (int l = 0; l < NP; ++l) w[r][l] = rb[row * PR + pi * K + l];
+        }
+        s_t_var<T, K, 1, RB>(variant_of(vx, N), c, w, z);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int i = 0; i < NP; ++i) z[r][i] = 0;
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int row = g + r * GR;
+        if (row < RN)
+#pragma unroll
+          for (int i = 0; i < NP; ++i) z1[row * PE + pi * NP + i] = z[r][i];
+      }
     }
-#pragma unroll
-    for (int i = 0; i < NP; ++i) z1[r * PE + pi * NP + i] = z[i];
-  }
-  __syncthreads();
+    __syncthreads();
 
-  // FY: per column (vx, i_x): march over patch rows vy = cy0..cy0+C: gather S_vy^T, divide by
-  // lambda_vy + lambda_vx, scatter S_vy into row accumulators; emit completed owned rows.
-  for (int col = tid; col < E; col += blockDim.x) {
-    const int pi = col / NP, ix = col % NP;
-    const int64_t vx = cx0 + pi;
-    const bool vx_ok = (vx >= 1 && vx <= N - 1);
-    const int varx = vx_ok ? variant_of(vx, N) : 1;
-    const T lx = P.c.lam[varx][ix];
-    T inv1[NP];
-#pragma unroll
-    for (int i = 0; i < NP; ++i) inv1[i] = T(1) / (P.c.lam[1][i] + lx);
-    T acc[NP];
-#pragma unroll
-    for (int l = 0; l < NP; ++l) acc[l] = 0;
-    for (int qi = 0; qi <= C; ++qi) {
+    // FYg: lanes <-> column groups, one patch row vy per unit
+#pragma unroll 1
+    for (int it = 0; it < cdiv(GE * (C + 1), NT); ++it, ++round) {
+      const int u = it * NT + tid;
+      if (u >= GE * (C + 1)) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      const int g = u % GE, qi = u / GE;
       const int64_t vy = cy0 + qi;
-      if (vx_ok && vy >= 1 && vy <= N - 1) {
-        T w[NP], z[NP];
+      int col[RB];
 #pragma unroll
-        for (int l = 0; l < NP; ++l) w[l] = z1[(qi * K + l) * PE + col];
+      for (int r = 0; r < RB; ++r) col[r] = min(g + r * GE, E - 1);
+      T z[RB][NP];
+      if (vy >= 1 && vy <= N - 1) {
+        T w[RB][NP];
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int l = 0; l < NP; ++l) w[r][l] = z1[(qi * K + l) * PE + col[r]];
         const int vary = variant_of(vy, N);
-        if (vary == 1) {
-          s_t<T, K, 1>(P.c, w, z);
+        s_t_var<T, K, 1, RB>(vary, c, w, z);
 #pragma unroll
-          for (int i = 0; i < NP; ++i) z[i] *= inv1[i];
-          s_n<T, K, 1>(P.c, z, acc);
-        } else if (vary == 0) {
-          s_t<T, K, 0>(P.c, w, z);
+        for (int r = 0; r < RB; ++r) {
+          const int pi = col[r] / NP, ix = col[r] - (col[r] / NP) * NP;
+          const int64_t vx = cx0 + pi;
+          if (vx < 1 || vx > N - 1) {
 #pragma unroll
-          for (int i = 0; i < NP; ++i) z[i] /= (P.c.lam[0][i] + lx);
-          s_n<T, K, 0>(P.c, z, acc);
-        } else {
-          s_t<T, K, 2>(P.c, w, z);
+            for (int i = 0; i < NP; ++i) z[r][i] = 0;
+          } else if (vary == 1 && variant_of(vx, N) == 1) {
 #pragma unroll
-          for (int i = 0; i < NP; ++i) z[i] /= (P.c.lam[2][i] + lx);
-          s_n<T, K, 2>(P.c, z, acc);
+            for (int i = 0; i < NP; ++i) z[r][i] *= invd[i * NP + ix];
+          } else {
+            const T lx = P.c.lam[variant_of(vx, N)][ix];
+#pragma unroll
+            for (int i = 0; i < NP; ++i) z[r][i] /= (P.c.lam[vary][i] + lx);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int i = 0; i < NP; ++i) z[r][i] = 0;
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int cc = g + r * GE;
+        if (cc < E)
+#pragma unroll
+          for (int i = 0; i < NP; ++i) z2[(qi * NP + i) * PE + cc] = z[r][i];
+      }
+    }
+    __syncthreads();
+
+    // FYs: lanes <-> column groups, one cell row cy per unit: rows cyK .. cyK+K-1
+#pragma unroll 1
+    for (int it = 0; it < cdiv(GE * C, NT); ++it, ++round) {
+      const int u = it * NT + tid;
+      if (u >= GE * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      const int g = u % GE, ci = u / GE;
+      T a0[RB][NP], a1[RB][NP], out[RB][K];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int cc = min(g + r * GE, E - 1);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          a0[r][i] = z2[(ci * NP + i) * PE + cc];
+          a1[r][i] = z2[((ci + 1) * NP + i) * PE + cc];
         }
       }
-      // rows (vy-1)K+1 .. vy K are complete: emit the owned ones, then shift by K
+      cell_from_patches<T, K, RB>(c, cy0 + ci, N, a0, a1, out);
 #pragma unroll
-      for (int l = 0; l < K; ++l) {
-        const int64_t ny = (vy - 1) * K + 1 + l;
-        const int64_t o = ny - cy0 * K;
-        if (o >= 0 && o < O) z3[o * PE + col] = acc[l];
-      }
+      for (int r = 0; r < RB; ++r) {
+        const int cc = g + r * GE;
+        if (cc < E)
 #pragma unroll
-      for (int l = 0; l < NP; ++l) acc[l] = (l + K < NP) ? acc[l + K] : T(0);
-    }
-  }
-  __syncthreads();
-
-  // FS: out[y][cx K + p] = sum_i S_cx[K-1+p][i] Z3[y][cx][i] + sum_i S_{cx+1}[p-1][i] Z3[y][cx+1][i]
-  T* outs = rb;                                  // [O][PS] staging (rb is dead)
-  for (int u = tid; u < O * C; u += blockDim.x) {
-    const int oy = u % O, ci = u / O;
-    const int64_t cx = cx0 + ci;
-    T out[K];
-#pragma unroll
-    for (int p = 0; p < K; ++p) out[p] = 0;
-    if (cx < N) {
-      T z0[NP], z1v[NP];
-#pragma unroll
-      for (int i = 0; i < NP; ++i) {
-        z0[i] = z3[oy * PE + ci * NP + i];
-        z1v[i] = z3[oy * PE + (ci + 1) * NP + i];
-      }
-      if (cx >= 1) {                       // patch cx: local rows K-1 .. 2K-2
-        const int v0 = variant_of(cx, N);
-        if (v0 == 1) s_rows<T, K, 1, K - 1, 0>(P.c, z0, out);
-        else if (v0 == 0) s_rows<T, K, 0, K - 1, 0>(P.c, z0, out);
-        else s_rows<T, K, 2, K - 1, 0>(P.c, z0, out);
-      }
-      if (cx + 1 <= N - 1) {               // patch cx+1: local rows p-1 for p >= 1
-        const int v1 = variant_of(cx + 1, N);
-        if (v1 == 1) s_rows<T, K, 1, -1, 1>(P.c, z1v, out);
-        else if (v1 == 0) s_rows<T, K, 0, -1, 1>(P.c, z1v, out);
-        else s_rows<T, K, 2, -1, 1>(P.c, z1v, out);
+          for (int p = 0; p < K; ++p) z3[(ci * K + p) * PE + cc] = out[r][p];
       }
     }
-#pragma unroll
-    for (int p = 0; p < K; ++p) outs[oy * PS + ci * K + p] = out[p];
-  }
-  __syncthreads();
+    __syncthreads();
 
-  for (int e = tid; e < O * O; e += blockDim.x) {
-    const int oy = e / O, ox = e % O;
-    const int64_t jy = cy0 * K + oy, jx = cx0 * K + ox;
-    if (jx < 1 || jx > KN - 1 || jy < 1 || jy > KN - 1) continue;
-    const int64_t g = (jy - 1) * n + (jx - 1);
-    P.x[g] = fma(P.factor, outs[oy * PS + ox], P.x[g]);
+    // FS: lanes <-> row groups, one cell column cx per unit
+#pragma unroll 1
+    for (int it = 0; it < cdiv(GO * C, NT); ++it, ++round) {
+      const int u = it * NT + tid;
+      if (u >= GO * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      const int g = u % GO, ci = u / GO;
+      T a0[RB][NP], a1[RB][NP], out[RB][K];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int oy = min(g + r * GO, O - 1);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          a0[r][i] = z3[oy * PE + ci * NP + i];
+          a1[r][i] = z3[oy * PE + (ci + 1) * NP + i];
+        }
+      }
+      cell_from_patches<T, K, RB>(c, cx0 + ci, N, a0, a1, out);
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int oy = g + r * GO;
+        if (oy < O)
+#pragma unroll
+          for (int p = 0; p < K; ++p) outs[oy * PS + ci * K + p] = out[r][p];
+      }
+    }
+    __syncthreads();
+
+    for (int e = tid; e < O * O; e += NT) {
+      const int oy = e / O, ox = e - (e / O) * O;
+      const int64_t jy = cy0 * K + oy, jx = cx0 * K + ox;
+      if (jx < 1 || jx > KN - 1 || jy < 1 || jy > KN - 1) continue;
+      P.x[(jy - 1) * n + (jx - 1)] = fma(P.factor, outs[oy * PS + ox], xt[oy * PS + ox]);
+    }
+    __syncthreads();
+    buf ^= 1;
   }
 }
 
@@ -484,40 +714,53 @@ const std::vector<double>& coef_of<double>(const FusedLevel& F) { return F.c64; 
 template <>
 const std::vector<float>& coef_of<float>(const FusedLevel& F) { return F.c32; }
 
+template <typename KernelT>
+static int persistent_grid(KernelT kern, size_t smem, int ntiles) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, smem);
+  return std::max(1, std::min(ntiles, sms * std::max(per, 1)));
+}
+
 template <typename T, int K>
 static void launch_apply(const FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st) {
-  constexpr int C = Tile<K>::C, O = Tile<K>::O;
-  constexpr int BW = (C + 3) * K + 1;
-  const size_t smem = sizeof(T) * (size_t(BW) * odd(BW) + 3 * size_t(BW) * odd(O));
-  static bool attr = false;
-  if (!attr) {
+  using LY = ApplyLayout<T, K>;
+  const size_t smem = sizeof(T) * size_t(LY::TOTAL);
+  static int grid_cache = -1;
+  const int ntx = int((F.N + LY::C - 1) / LY::C);
+  if (grid_cache < 0) {
     cudaFuncSetAttribute(apply2d_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    cudaFuncSetAttribute(apply2d_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    grid_cache = persistent_grid(apply2d_kernel<T, K>, smem, 1 << 30);
   }
   ApplyP<T, K> p;
   std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
   p.x = x; p.b = b; p.y = y; p.N = F.N; p.n = F.n;
   p.scale = T(1.0 / (F.h * F.h));
-  const unsigned g = unsigned((F.N + C - 1) / C);
-  apply2d_kernel<T, K><<<dim3(g, g), 256, smem, st>>>(p);
+  p.zero = 0;
+  const int grid = std::min(grid_cache, ntx * ntx);
+  apply2d_kernel<T, K><<<grid, 256, smem, st>>>(p);
 }
 
 template <typename T, int K>
 static void launch_fdm(const FusedLevel& F, T omega, const T* r, T* x, cudaStream_t st) {
-  constexpr int C = Tile<K>::C, O = Tile<K>::O, NP = 2 * K - 1;
-  constexpr int RN = (C + 2) * K - 1, E = (C + 1) * NP;
-  const size_t smem = sizeof(T) * (size_t(RN) * odd(RN) + size_t(RN) * odd(E) + size_t(O) * odd(E));
-  static bool attr = false;
-  if (!attr) {
+  using LY = FdmLayout<T, K>;
+  const size_t smem = sizeof(T) * size_t(LY::TOTAL);
+  static int grid_cache = -1;
+  const int ntx = int((F.N + LY::C - 1) / LY::C);
+  if (grid_cache < 0) {
     cudaFuncSetAttribute(fdm2d_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    cudaFuncSetAttribute(fdm2d_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    grid_cache = persistent_grid(fdm2d_kernel<T, K>, smem, 1 << 30);
   }
   FdmP<T, K> p;
   std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
   p.r = r; p.x = x; p.N = F.N; p.n = F.n;
   p.factor = T(double(omega) * F.h * F.h);
-  const unsigned g = unsigned((F.N + C - 1) / C);
-  fdm2d_kernel<T, K><<<dim3(g, g), 256, smem, st>>>(p);
+  p.zero = 0;
+  const int grid = std::min(grid_cache, ntx * ntx);
+  fdm2d_kernel<T, K><<<grid, 256, smem, st>>>(p);
 }
 
 template <typename T>
