@@ -311,7 +311,7 @@ def main():
         alt = {"bound": "alu", "achieved": round(ach_tf, 3), "peak": round(peak_alu, 2), "unit": "TFLOP/s",
                "frac": round(f_alu, 4)}
     roof["kernel"] = kern
-    roof["traffic"] = traffic_from_profiles(f"{kern}_k{k}_{args.dtype}")
+    roof["traffic"] = traffic_from_profiles(f"{kern}_kernel_k{k}_{args.dtype}")
     roof["peak_source"] = f"hbm {peak_src} (MEASURED_PEAKS.json); alu derived 148x{64 if esz == 8 else 128}x2 flop/clk at {clk_mhz:.0f} MHz (DESIGN.md)"
     roof["alt"] = alt
     roof["launch_ms"] = round(t_k, 4)
