@@ -13,8 +13,9 @@ e2e    = the same step through the C ABI with host buffers: x, b copied from pin
 Extras: matvec GDoF/s on the same mesh, per-kernel roofline of the dominant kernel, an MG-PCG
 time-to-solve (FP64 vs FP32 V-cycle, nested mesh) and the CPU oracle baseline.
 
-Multi-GPU (torchrun, --gpus N): every rank runs its own copy of the workload (replicas, no
-data-path collective yet), timing is the max over ranks.
+Multi-GPU (torchrun, --gpus N): weak scaling on a y-slab decomposition of a global mesh with
+~16.7M DoFs per GPU; every step exchanges ghost rows between neighbours (NCCL send/recv) before
+the slab smoothing step; timing is the max over ranks.
 --impl reference: times the CPU oracle (oracle/) on a bounded sample of the same workload.
 """
 import argparse
@@ -186,6 +187,92 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def run_slabs(args, world, rank, local):
+    """Weak scaling over `world` GPUs: global 2D mesh of N = round(N_k sqrt(world)) cells per axis cut into
+    slabs along y; per step every rank exchanges its 4k-2 ghost rows with its neighbours
+    (NCCL send/recv through torch.distributed) and runs the slab smoothing step on its owned rows."""
+    import math
+    import torch
+    import torch.distributed as dist
+    from paper_2412_05082_b200 import api
+    from paper_2412_05082_b200.dist import partition, exchange_ghosts
+    k = args.degree
+    N = int(round(CFG2_CELLS[k] * math.sqrt(world)))
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    esz = 8 if dt == torch.float64 else 4
+    ctx = api.Context(2, k, 3, cells_override=N, device=local)
+    L = 3
+    n = k * N - 1
+    ga, _ = ctx.slab_ghosts()
+    s = partition(N, k, world, ga)[rank]
+    rng = torch.Generator(device="cpu").manual_seed(20241205 + rank)
+    xw = (torch.rand(s.lrows * n, generator=rng, dtype=torch.float64) * 2 - 1).to("cuda", dt)
+    bw = (torch.rand(s.lrows * n, generator=rng, dtype=torch.float64) * 2 - 1).to("cuda", dt)
+    rw = torch.empty_like(xw)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        exchange_ghosts(xw, s, n)
+        ctx.slab_avs_step(L, 0.25, s.row0, s.lrows, s.own_lo, s.own_hi, bw, xw, rw)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    lc0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    t_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    launches = ctx.launch_count() - lc0
+    own_rows = s.own_hi - s.own_lo
+    total_dofs = n * n
+
+    # e2e: owned rows of x, b from pinned host memory each step, owned x' back
+    xh = xw.view(-1, n)[s.own_local].cpu().contiguous().pin_memory()
+    bh = bw.view(-1, n)[s.own_local].cpu().contiguous().pin_memory()
+    oh = torch.empty_like(xh).pin_memory()
+
+    def e2e_step():
+        xw.view(-1, n)[s.own_local].copy_(xh, non_blocking=True)
+        bw.view(-1, n)[s.own_local].copy_(bh, non_blocking=True)
+        step()
+        oh.copy_(xw.view(-1, n)[s.own_local], non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    line = {
+        "metric": METRIC, "value": round(total_dofs / (t_ms * 1e-3) / 1e9, 3), "unit": "GDoF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": {"workload": f"cfg2 weak-scaled: 2D unit square, Q{k} C0IP, N={N} cells/axis ({total_dofs} DoFs, "
+                               f"~{total_dofs // world} per GPU), one additive smoothing step per rank on a y-slab "
+                               f"with {ga} NCCL-exchanged ghost rows per side",
+                   "degree": k, "cells": N, "parallelism": f"slab{world}", "ghost_rows": ga,
+                   "l2": "inputs larger than L2"},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+        "e2e": {"value": round(total_dofs / (t_e2e * 1e-3) / 1e9, 3), "unit": "GDoF/s",
+                "h2d_bytes_per_step": 2 * own_rows * n * esz, "d2h_bytes_per_step": own_rows * n * esz},
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    ctx.close()
+    dist.destroy_process_group()
+
+
 def traffic_from_profiles(kernel_key):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -216,6 +303,8 @@ def main():
     from paper_2412_05082_b200 import api
 
     k = args.degree
+    if world > 1:
+        return run_slabs(args, world, rank, local)
     N = CFG2_CELLS[k]
     dt = torch.float64 if args.dtype == "f64" else torch.float32
     ctx = api.Context(2, k, 3, cells_override=N, device=local)

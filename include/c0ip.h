@@ -160,6 +160,31 @@ c0ip_status c0ip_pcg(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, do
                      double rtol, int32_t max_iter, c0ip_report* rep, double* res_history,
                      void* stream);
 
+/* ---- Slab (multi-GPU) entry points, SURVEY.md §8e -------------------------------------------------
+ * The mesh is split into slabs along the slowest axis (y in 2D, z in 3D); each rank (one process per
+ * GPU) holds a window of global interior rows [row0, row0 + lrows) of that axis in a contiguous array
+ * (a "row" is n_1d^(d-1) values, x fastest) and owns the node rows [out_lo, out_hi) (node row
+ * j = interior row + 1).  The caller fills the ghost rows of x_ext before each call (halo exchange, e.g.
+ * NCCL send/recv through torch.distributed; paper_2412_05082_b200/dist.py).  Results are bitwise equal
+ * to the single-domain call on the owned rows.  STATE if the level has no slab-capable kernel (2D levels
+ * with N >= 8 in this release). */
+
+/* Ghost rows a slab call needs on each side of [out_lo, out_hi) (clipped at the domain boundary):
+ * AVS step: 4k-2 (residual on the owned rows +- (2k-2), each needing x +- 2k); apply: 2k. */
+c0ip_status c0ip_slab_ghosts(c0ip_ctx ctx, int32_t* ghost_avs, int32_t* ghost_apply);
+
+/* One additive smoothing step on the owned rows: r_ext (scratch, same window) gets
+ * b - A x on the owned rows +- (2k-2), then x_ext is updated in place on the owned rows.  b_ext may be
+ * NULL-free only; ARG if the window does not hold the required ghost rows. */
+c0ip_status c0ip_slab_avs_step(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, double omega, int64_t row0,
+                               int64_t lrows, int64_t out_lo, int64_t out_hi, const void* b_ext,
+                               void* x_ext, void* r_ext, void* stream);
+
+/* y = A x (b_ext == NULL) or r = b - A x on the owned rows of a slab window (ghosts of width 2k). */
+c0ip_status c0ip_slab_apply(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, int64_t row0, int64_t lrows,
+                            int64_t out_lo, int64_t out_hi, const void* b_ext, const void* x_ext,
+                            void* y_ext, void* stream);
+
 /* Number of kernels this context has launched since creation (for the bench's gpu_launches). */
 c0ip_status c0ip_launch_count(c0ip_ctx ctx, int64_t* count);
 

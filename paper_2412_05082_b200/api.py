@@ -157,3 +157,21 @@ class Context:
         report = dict(iterations=rep.iterations, converged=bool(rep.converged), r0=rep.r0, rn=rep.rn, nu=rep.nu,
                       seconds=rep.seconds)
         return x, report, hist[: rep.iterations + 1]
+
+    # ------------------------------------------------------------------ slab (multi-GPU) calls
+    def slab_ghosts(self):
+        ga, gp = C.c_int32(), C.c_int32()
+        L.check(self._lib.c0ip_slab_ghosts(self.h, C.byref(ga), C.byref(gp)))
+        return ga.value, gp.value
+
+    def slab_avs_step(self, level, omega, row0, lrows, out_lo, out_hi, b_ext, x_ext, r_ext):
+        L.check(self._lib.c0ip_slab_avs_step(self.h, level, _dtype(x_ext), float(omega), int(row0), int(lrows),
+                                             int(out_lo), int(out_hi), _ptr(b_ext), _ptr(x_ext), _ptr(r_ext),
+                                             _stream()))
+        return x_ext
+
+    def slab_apply(self, level, row0, lrows, out_lo, out_hi, x_ext, y_ext, b_ext=None):
+        L.check(self._lib.c0ip_slab_apply(self.h, level, _dtype(x_ext), int(row0), int(lrows), int(out_lo),
+                                          int(out_hi), _ptr(b_ext) if b_ext is not None else None, _ptr(x_ext),
+                                          _ptr(y_ext), _stream()))
+        return y_ext

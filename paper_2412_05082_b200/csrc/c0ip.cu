@@ -307,7 +307,8 @@ void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, b
         int64_t cnt = L.color_off[c + 1] - L.color_off[c];
         if (cnt == 0) continue;
         if (ctx->path == C0IP_PATH_AUTO && L.fused &&
-            c0ip::fused_mvs_color<T>(*L.fused, c, omega, b, x, st, &ctx->launches))
+            c0ip::fused_mvs_color<T>(*L.fused, L.colors_d.p + L.color_off[c], cnt, omega, b, x, st,
+                                     &ctx->launches))
           continue;
         apply_op<T>(ctx, L, x, b, t.sres.p, st);                 // residual per colour
         patch_solve<T>(ctx, L, t.sres.p, x, omega, L.colors_d.p + L.color_off[c], cnt, 0, st);
@@ -848,6 +849,73 @@ c0ip_status c0ip_pcg(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, do
     rep->nu = (it == 0 || ratio <= 0) ? 0.0 : -8.0 / std::log10(std::pow(ratio, 1.0 / it));
     rep->seconds = std::chrono::duration<double>(t1 - t0).count();
   }
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_slab_ghosts(c0ip_ctx ctx, int32_t* ghost_avs, int32_t* ghost_apply) {
+  if (!ctx) return fail(C0IP_ERR_ARG, "null context");
+  if (ghost_avs) *ghost_avs = 4 * ctx->k - 2;
+  if (ghost_apply) *ghost_apply = 2 * ctx->k;
+  return C0IP_OK;
+}
+
+static c0ip_status check_window(c0ip_ctx ctx, Level& L, int64_t row0, int64_t lrows, int64_t out_lo,
+                                int64_t out_hi, int64_t ghost) {
+  const int64_t KN = int64_t(ctx->k) * L.N;
+  if (row0 < 0 || lrows < 1 || row0 + lrows > L.n) return fail(C0IP_ERR_ARG, "slab window outside the level");
+  if (out_lo < 1 || out_hi > KN || out_lo > out_hi) return fail(C0IP_ERR_ARG, "owned rows outside the level");
+  const int64_t need_lo = std::max<int64_t>(1, out_lo - ghost), need_hi = std::min<int64_t>(KN - 1, out_hi - 1 + ghost);
+  if (row0 + 1 > need_lo || row0 + lrows < need_hi)
+    return fail(C0IP_ERR_ARG, "slab window lacks ghost rows (need node rows [" + std::to_string(need_lo) + ", " +
+                                  std::to_string(need_hi) + "])");
+  if (!L.fused || !c0ip::fused_supports_slab(*L.fused))
+    return fail(C0IP_ERR_STATE, "slab calls need a fused (2D, N >= 8) level");
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_slab_avs_step(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, double omega, int64_t row0,
+                               int64_t lrows, int64_t out_lo, int64_t out_hi, const void* b_ext, void* x_ext,
+                               void* r_ext, void* stream) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (!b_ext || !x_ext || !r_ext) return fail(C0IP_ERR_ARG, "null vector");
+  Level& L = ctx->levels[level];
+  if ((s = check_window(ctx, L, row0, lrows, out_lo, out_hi, 4 * ctx->k - 2))) return s;
+  ABI_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t KN = int64_t(ctx->k) * L.N, gr = 2 * ctx->k - 2;
+  c0ip::SlabWindow wr{row0, lrows, std::max<int64_t>(1, out_lo - gr), std::min<int64_t>(KN, out_hi + gr)};
+  c0ip::SlabWindow wo{row0, lrows, out_lo, out_hi};
+  if (dt == C0IP_F64) {
+    c0ip::fused_apply<double>(*L.fused, (const double*)x_ext, (const double*)b_ext, (double*)r_ext, st, &ctx->launches, &wr);
+    c0ip::fused_fdm<double>(*L.fused, omega, (const double*)r_ext, (double*)x_ext, st, &ctx->launches, &wo);
+  } else if (dt == C0IP_F32) {
+    c0ip::fused_apply<float>(*L.fused, (const float*)x_ext, (const float*)b_ext, (float*)r_ext, st, &ctx->launches, &wr);
+    c0ip::fused_fdm<float>(*L.fused, (float)omega, (const float*)r_ext, (float*)x_ext, st, &ctx->launches, &wo);
+  } else {
+    return fail(C0IP_ERR_ARG, "bad dtype");
+  }
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_slab_apply(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, int64_t row0, int64_t lrows, int64_t out_lo,
+                            int64_t out_hi, const void* b_ext, const void* x_ext, void* y_ext, void* stream) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (!x_ext || !y_ext) return fail(C0IP_ERR_ARG, "null vector");
+  Level& L = ctx->levels[level];
+  if ((s = check_window(ctx, L, row0, lrows, out_lo, out_hi, 2 * ctx->k))) return s;
+  ABI_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  c0ip::SlabWindow w{row0, lrows, out_lo, out_hi};
+  if (dt == C0IP_F64)
+    c0ip::fused_apply<double>(*L.fused, (const double*)x_ext, (const double*)b_ext, (double*)y_ext, st, &ctx->launches, &w);
+  else if (dt == C0IP_F32)
+    c0ip::fused_apply<float>(*L.fused, (const float*)x_ext, (const float*)b_ext, (float*)y_ext, st, &ctx->launches, &w);
+  else
+    return fail(C0IP_ERR_ARG, "bad dtype");
   return C0IP_OK;
   ABI_CATCH
 }

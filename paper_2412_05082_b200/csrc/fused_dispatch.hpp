@@ -21,13 +21,25 @@ std::unique_ptr<FusedLevel, FusedLevelDeleter> make_fused_level_impl(int d, int 
                                                                      const RefData& ref,
                                                                      const Fdm& fdm, double h);
 
+// Slab window (multi-GPU z-slabs): arrays hold global interior rows [row0, row0 + lrows) of the slowest
+// axis; outputs are written for node rows j in [out_lo, out_hi).  nullptr = the whole domain.
+struct SlabWindow {
+  int64_t row0, lrows, out_lo, out_hi;
+};
+bool fused_supports_slab(const FusedLevel& F);
+
 template <typename T>
-bool fused_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches);
+bool fused_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches,
+                 const SlabWindow* win = nullptr);
+template <typename T>
+bool fused_fdm(FusedLevel& F, T omega, const T* r, T* x, cudaStream_t st, int64_t* launches,
+               const SlabWindow* win = nullptr);
 template <typename T>
 bool fused_avs(FusedLevel& F, T omega, const T* b, T* x, T* scratch, cudaStream_t st,
                int64_t* launches);
+// one colour of the coloured MVS (patch list of the colour on the device)
 template <typename T>
-bool fused_mvs_color(FusedLevel& F, int color, T omega, const T* b, T* x, cudaStream_t st,
-                     int64_t* launches);
+bool fused_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega, const T* b, T* x,
+                     cudaStream_t st, int64_t* launches);
 
 }  // namespace c0ip

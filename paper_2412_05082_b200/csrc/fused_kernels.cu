@@ -57,6 +57,8 @@ struct ApplyP {
   int64_t N, n;             // cells, 1D interior dofs (n = KN-1)
   T scale;                  // h^-2
   int zero;                 // 0 at run time (opaque to the compiler)
+  int64_t row0, lrows;      // slab window: local row 0 = global interior row row0; lrows rows held
+  int64_t out_lo, out_hi;   // node rows j (= interior row + 1) to write, [out_lo, out_hi)
 };
 
 template <typename T, int K>
@@ -67,6 +69,8 @@ struct FdmP {
   int64_t N, n;
   T factor;                 // omega * h^2
   int zero;
+  int64_t row0, lrows;      // slab window (see ApplyP)
+  int64_t out_lo, out_hi;
 };
 
 template <int K>
@@ -156,12 +160,15 @@ __device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem, bool pred)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
-// ROWS x COLS box of nodes starting at node (Y0, X0) into smem with row pitch PITCH
+// ROWS x COLS box of nodes starting at node (Y0, X0) into smem with row pitch PITCH.  Global node
+// rows are held in a slab window: node row jy lives at local interior row jy - 1 - row0, valid for
+// local rows [0, lrows); everything else (clamped boundary, outside the window) is zero-filled.
 template <typename T, int ROWS, int COLS, int PITCH>
 __device__ __forceinline__ void load_box_async(T* dst, const T* src, int64_t n, int64_t KN, int64_t Y0,
-                                               int64_t X0) {
-  const bool inner = (X0 >= 1 && X0 + COLS - 1 <= KN - 1 && Y0 >= 1 && Y0 + ROWS - 1 <= KN - 1);
-  const T* base = src + (Y0 - 1) * n + (X0 - 1);
+                                               int64_t X0, int64_t row0, int64_t lrows) {
+  const int64_t ylo = (row0 + 1 > 1) ? row0 + 1 : int64_t(1), yhi = (row0 + lrows < KN - 1) ? row0 + lrows : KN - 1;
+  const bool inner = (X0 >= 1 && X0 + COLS - 1 <= KN - 1 && Y0 >= ylo && Y0 + ROWS - 1 <= yhi);
+  const T* base = src + (Y0 - 1 - row0) * n + (X0 - 1);
   if (inner) {
     for (int e = threadIdx.x; e < ROWS * COLS; e += blockDim.x) {
       const int r = e / COLS, c = e - (e / COLS) * COLS;
@@ -171,10 +178,17 @@ __device__ __forceinline__ void load_box_async(T* dst, const T* src, int64_t n, 
     for (int e = threadIdx.x; e < ROWS * COLS; e += blockDim.x) {
       const int r = e / COLS, c = e - (e / COLS) * COLS;
       const int64_t jy = Y0 + r, jx = X0 + c;
-      const bool ok = (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1);
+      const bool ok = (jx >= 1 && jx <= KN - 1 && jy >= ylo && jy <= yhi);
       cp_async_elem(dst + r * PITCH + c, ok ? base + (int64_t)r * n + c : src, ok);
     }
   }
+}
+
+// tile rows covering node rows [out_lo, out_hi): ty in [ty0, ty1)
+template <int K, int C>
+__device__ __forceinline__ void tile_rows(int64_t out_lo, int64_t out_hi, int& ty0, int& ty1) {
+  ty0 = int((out_lo / K) / C);
+  ty1 = int(((out_hi - 1) / K) / C) + 1;
 }
 
 // ----------------------------------------------------------------------------- apply2d
@@ -205,13 +219,15 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
   T* sM = sL + LY::STAGE;
   const int64_t N = P.N, n = P.n, KN = K * N;
   const int ntx = int((N + C - 1) / C);
-  const int ntiles = ntx * ntx;
+  int ty0, ty1;
+  tile_rows<K, C>(P.out_lo, P.out_hi, ty0, ty1);
+  const int ntiles = ntx * (ty1 - ty0);
   const int tid = threadIdx.x;
 
   auto issue = [&](int t, int buf) {
-    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(t / ntx) * C;
-    load_box_async<T, BW, BW, PX>(xbuf0 + buf * LY::XB, P.x, n, KN, (cy0 - 2) * K, (cx0 - 2) * K);
-    if (P.b) load_box_async<T, O, O, PO>(bbuf0 + buf * LY::BB, P.b, n, KN, cy0 * K, cx0 * K);
+    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(ty0 + t / ntx) * C;
+    load_box_async<T, BW, BW, PX>(xbuf0 + buf * LY::XB, P.x, n, KN, (cy0 - 2) * K, (cx0 - 2) * K, P.row0, P.lrows);
+    if (P.b) load_box_async<T, O, O, PO>(bbuf0 + buf * LY::BB, P.b, n, KN, cy0 * K, cx0 * K, P.row0, P.lrows);
   };
 
   int buf = 0, round = 0;
@@ -224,7 +240,7 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
     __syncthreads();
     const T* xb = xbuf0 + buf * LY::XB;
     const T* bt = bbuf0 + buf * LY::BB;
-    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(t / ntx) * C;
+    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(ty0 + t / ntx) * C;
 
     // x-stage: B^_x x, L^_x x, M^_x x on all box rows, owned columns.  lanes <-> row groups;
     // a thread holds rows g, g + GX, ... (RB rows) of one cell and reuses every coefficient RB times.
@@ -346,9 +362,9 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
 #pragma unroll
         for (int p = 0; p < K; ++p) {
           const int64_t j = cy * K + p;
-          if (j < 1 || j > KN - 1) continue;
+          if (j < P.out_lo || j >= P.out_hi) continue;
           const T v = P.scale * acc[p][r];
-          P.y[(j - 1) * n + (jx - 1)] = P.b ? bt[(ci * K + p) * PO + cc] - v : v;
+          P.y[(j - 1 - P.row0) * n + (jx - 1)] = P.b ? bt[(ci * K + p) * PO + cc] - v : v;
         }
       }
     }
@@ -458,16 +474,19 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
   static_assert(RN >= O && LY::Z2 >= O * PS, "Z3 / staging do not fit");
   const int64_t N = P.N, n = P.n, KN = K * N;
   const int ntx = int((N + C - 1) / C);
-  const int ntiles = ntx * ntx;
+  int ty0, ty1;
+  tile_rows<K, C>(P.out_lo, P.out_hi, ty0, ty1);
+  const int ntiles = ntx * (ty1 - ty0);
   const int tid = threadIdx.x;
 
   for (int e = tid; e < NP * NP; e += blockDim.x)
     invd[e] = T(1) / (P.c.lam[1][e / NP] + P.c.lam[1][e % NP]);
 
   auto issue = [&](int t, int buf) {
-    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(t / ntx) * C;
-    load_box_async<T, RN, RN, PR>(rbuf0 + buf * LY::RB_, P.r, n, KN, (cy0 - 1) * K + 1, (cx0 - 1) * K + 1);
-    load_box_async<T, O, O, PS>(xbuf0 + buf * LY::XT, P.x, n, KN, cy0 * K, cx0 * K);
+    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(ty0 + t / ntx) * C;
+    load_box_async<T, RN, RN, PR>(rbuf0 + buf * LY::RB_, P.r, n, KN, (cy0 - 1) * K + 1, (cx0 - 1) * K + 1,
+                                  P.row0, P.lrows);
+    load_box_async<T, O, O, PS>(xbuf0 + buf * LY::XT, P.x, n, KN, cy0 * K, cx0 * K, P.row0, P.lrows);
   };
 
   int buf = 0, round = 0;
@@ -480,7 +499,7 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
     __syncthreads();
     const T* rb = rbuf0 + buf * LY::RB_;
     const T* xt = xbuf0 + buf * LY::XT;
-    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(t / ntx) * C;
+    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(ty0 + t / ntx) * C;
 
     // FX: lanes <-> row groups, one patch vx per unit (uniform variant)
 #pragma unroll 1
@@ -627,11 +646,266 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
     for (int e = tid; e < O * O; e += NT) {
       const int oy = e / O, ox = e - (e / O) * O;
       const int64_t jy = cy0 * K + oy, jx = cx0 * K + ox;
-      if (jx < 1 || jx > KN - 1 || jy < 1 || jy > KN - 1) continue;
-      P.x[(jy - 1) * n + (jx - 1)] = fma(P.factor, outs[oy * PS + ox], xt[oy * PS + ox]);
+      if (jx < 1 || jx > KN - 1 || jy < P.out_lo || jy >= P.out_hi) continue;
+      P.x[(jy - 1 - P.row0) * n + (jx - 1)] = fma(P.factor, outs[oy * PS + ox], xt[oy * PS + ox]);
     }
     __syncthreads();
     buf ^= 1;
+  }
+}
+
+// ----------------------------------------------------------------------------- mvs2d
+// One colour of the coloured multiplicative smoother, patch-parallel and fused:
+// for every patch v of the colour (a batch of PB patches per CTA):
+//   r_v = (b - A x) on the (2k-1)^2 patch nodes, from the x box [(v-2)k, (v+2)k]^2 (the residual
+//         footprint: patch cells plus their face neighbours; identical to the global
+//         residual recomputed per colour because same-colour patches never touch each other's footprint),
+//   u_v = A~_v^{-1} r_v by FDM (S^T along x and y, divide by lambda_x + lambda_y, S along y and x),
+//   x  += omega u_v on the patch nodes (disjoint within a colour, plain stores).
+template <typename T, int K>
+struct MvsP {
+  Coef2<T, K> c;
+  T* x;
+  const T* b;
+  const int32_t* list;      // patch ids of the colour
+  int64_t count;
+  int64_t N, n;
+  T scale;                  // h^-2  (A = h^-2 A^)
+  T factor;                 // omega h^2 (A~^-1 = h^2 A^~^-1)
+  int zero;
+};
+
+template <typename T, int K>
+struct MvsLayout {
+  static constexpr int NP = 2 * K - 1, BX = 4 * K + 1;
+  static constexpr int PER = BX * BX + 3 * BX * NP + 2 * NP * NP;   // per patch
+  static constexpr int PB = (K <= 2) ? 32 : (K == 3) ? 16 : (K == 4) ? 12 : (K == 5) ? 8 : (K == 6) ? 6 : 4;
+  static constexpr int TOTAL = PB * PER;
+};
+
+template <typename T, int K>
+__global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ MvsP<T, K> P) {
+  using LY = MvsLayout<T, K>;
+  constexpr int NP = LY::NP, BX = LY::BX, PB = LY::PB, PER = LY::PER;
+  constexpr int NT = 256;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  const int64_t N = P.N, n = P.n, KN = K * N;
+  const int tid = threadIdx.x;
+  const int64_t first = (int64_t)blockIdx.x * PB;
+  int round = 0;
+  // per patch: xb [BX][BX] | sB, sL, sM [BX][NP] ; later rr [NP][NP] and z [NP][NP] alias xb
+  auto xb = [&](int p) { return sm + p * PER; };
+  auto sX = [&](int p, int which) { return sm + p * PER + BX * BX + which * BX * NP; };
+  auto rr = [&](int p) { return sm + p * PER + BX * BX + 3 * BX * NP; };
+  auto zz = [&](int p) { return rr(p) + NP * NP; };
+  auto vert = [&](int p, int64_t& vx, int64_t& vy) -> bool {
+    const int64_t q = first + p;
+    if (q >= P.count) return false;
+    const int64_t pid = P.list[q];
+    vx = 1 + pid % (N - 1);
+    vy = 1 + pid / (N - 1);
+    return true;
+  };
+
+  // 0. x boxes [(v-2)K, (v+2)K]^2 and b on the patch nodes
+  for (int e = tid; e < PB * BX * BX; e += NT) {
+    const int p = e / (BX * BX), rem = e - p * (BX * BX), r = rem / BX, cc = rem - (rem / BX) * BX;
+    int64_t vx, vy;
+    T v = 0;
+    if (vert(p, vx, vy)) {
+      const int64_t jy = (vy - 2) * K + r, jx = (vx - 2) * K + cc;
+      if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1) v = P.x[(jy - 1) * n + (jx - 1)];
+    }
+    xb(p)[r * BX + cc] = v;
+  }
+  for (int e = tid; e < PB * NP * NP; e += NT) {
+    const int p = e / (NP * NP), rem = e - p * (NP * NP), r = rem / NP, cc = rem - (rem / NP) * NP;
+    int64_t vx, vy;
+    T v = 0;
+    if (vert(p, vx, vy)) v = P.b[((vy - 1) * K + r) * n + ((vx - 1) * K + cc)];
+    rr(p)[r * NP + cc] = v;
+  }
+  __syncthreads();
+
+  // 1. x-stage on every box row, patch columns only: B^_x, L^_x, M^_x.  unit = (patch, box row).
+#pragma unroll 1
+  for (int it = 0; it < cdiv(PB * BX, NT); ++it, ++round) {
+    const int u = it * NT + tid;
+    if (u >= PB * BX) continue;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+    const int p = u / BX, r = u - (u / BX) * BX;
+    int64_t vx, vy;
+    if (!vert(p, vx, vy)) continue;
+    T w[BX];
+#pragma unroll
+    for (int q = 0; q < BX; ++q) w[q] = xb(p)[r * BX + q];
+    const bool edge = (vx == 1 || vx == N - 1);
+#pragma unroll
+    for (int l = 0; l < NP; ++l) {
+      // output node jx = (vx-1)K + 1 + l at box column K + 1 + l, class (1 + l) mod K
+      const int cb = K + 1 + l;
+      const int64_t jx = (vx - 1) * K + 1 + l;
+      const int s = edge ? special_row<K>(jx, N) : -1;
+      T ob = 0, ol = 0, om = 0;
+      with_p<K>((1 + l) % K, [&](auto PC) {
+        constexpr int PP = decltype(PC)::value;
+        auto body = [&](auto fb, auto fl, auto fm) {
+#pragma unroll
+          for (int q = 0; q <= 4 * K; ++q) {
+            const int col = cb + q - 2 * K;
+            if (col < 0 || col >= BX) continue;
+            if (!(PP == 0 || (q >= K - PP && q <= 4 * K - PP))) continue;
+            ob = fma(fb(q), w[col], ob);
+            if (q >= K && q <= 3 * K && (PP == 0 || (q - K >= K - PP && q - K <= 2 * K - PP))) {
+              ol = fma(fl(q), w[col], ol);
+              om = fma(fm(q), w[col], om);
+            }
+          }
+        };
+        if (s < 0)
+          body([&](int q) { return c.BI[PP][q]; }, [&](int q) { return c.LI[PP][q - K]; },
+               [&](int q) { return c.MI[PP][q - K]; });
+        else
+          body([&](int q) { return c.BS[s][q]; }, [&](int q) { return c.LS[s][q]; },
+               [&](int q) { return c.MS[s][q]; });
+      });
+      sX(p, 0)[r * NP + l] = ob;
+      sX(p, 1)[r * NP + l] = ol;
+      sX(p, 2)[r * NP + l] = om;
+    }
+  }
+  __syncthreads();
+
+  // 2. y-stage: r = b - h^-2 (B^_y(M^x) + M^_y(B^x) + 2 L^_y(L^x)) on the patch rows.  unit = (patch, col).
+#pragma unroll 1
+  for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
+    const int u = it * NT + tid;
+    if (u >= PB * NP) continue;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+    const int p = u / NP, l = u - (u / NP) * NP;
+    int64_t vx, vy;
+    if (!vert(p, vx, vy)) continue;
+    T wM[BX], wB[BX], wL[BX];
+#pragma unroll
+    for (int q = 0; q < BX; ++q) {
+      wM[q] = sX(p, 2)[q * NP + l];
+      wB[q] = sX(p, 0)[q * NP + l];
+      wL[q] = sX(p, 1)[q * NP + l];
+    }
+    const bool edge = (vy == 1 || vy == N - 1);
+#pragma unroll
+    for (int m = 0; m < NP; ++m) {
+      const int cb = K + 1 + m;
+      const int64_t jy = (vy - 1) * K + 1 + m;
+      const int s = edge ? special_row<K>(jy, N) : -1;
+      T v = 0;
+      with_p<K>((1 + m) % K, [&](auto PC) {
+        constexpr int PP = decltype(PC)::value;
+        auto body = [&](auto fb, auto fl, auto fm) {
+#pragma unroll
+          for (int q = 0; q <= 4 * K; ++q) {
+            const int row = cb + q - 2 * K;
+            if (row < 0 || row >= BX) continue;
+            if (!(PP == 0 || (q >= K - PP && q <= 4 * K - PP))) continue;
+            v = fma(fb(q), wM[row], v);
+            if (q >= K && q <= 3 * K && (PP == 0 || (q - K >= K - PP && q - K <= 2 * K - PP))) {
+              v = fma(fm(q), wB[row], v);
+              v = fma(T(2) * fl(q), wL[row], v);
+            }
+          }
+        };
+        if (s < 0)
+          body([&](int q) { return c.BI[PP][q]; }, [&](int q) { return c.LI[PP][q - K]; },
+               [&](int q) { return c.MI[PP][q - K]; });
+        else
+          body([&](int q) { return c.BS[s][q]; }, [&](int q) { return c.LS[s][q]; },
+               [&](int q) { return c.MS[s][q]; });
+      });
+      rr(p)[m * NP + l] = rr(p)[m * NP + l] - P.scale * v;
+    }
+  }
+  __syncthreads();
+
+  // 3. FDM: FX rows (S_vx^T), FY columns (S_vy^T, divide, S_vy), FS rows (S_vx) + update.
+#pragma unroll 1
+  for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
+    const int u = it * NT + tid;
+    if (u >= PB * NP) continue;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+    const int p = u / NP, i = u - (u / NP) * NP;
+    int64_t vx, vy;
+    if (!vert(p, vx, vy)) continue;
+    T w[1][NP], z[1][NP];
+#pragma unroll
+    for (int l = 0; l < NP; ++l) w[0][l] = rr(p)[i * NP + l];
+    s_t_var<T, K, 1, 1>(variant_of(vx, N), c, w, z);
+#pragma unroll
+    for (int l = 0; l < NP; ++l) zz(p)[i * NP + l] = z[0][l];
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
+    const int u = it * NT + tid;
+    if (u >= PB * NP) continue;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+    const int p = u / NP, j = u - (u / NP) * NP;
+    int64_t vx, vy;
+    if (!vert(p, vx, vy)) continue;
+    T w[1][NP], z[1][NP];
+#pragma unroll
+    for (int l = 0; l < NP; ++l) w[0][l] = zz(p)[l * NP + j];
+    const int vary = variant_of(vy, N), varx = variant_of(vx, N);
+    s_t_var<T, K, 1, 1>(vary, c, w, z);
+    const T lx = P.c.lam[varx][j];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) z[0][i] /= (P.c.lam[vary][i] + lx);
+    // S_vy z  -> column j
+#pragma unroll
+    for (int l = 0; l < NP; ++l) {
+      T s = 0;
+      if (vary == 1) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) s = fma(c.S[1][l * NP + i], z[0][i], s);
+      } else if (vary == 0) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) s = fma(c.S[0][l * NP + i], z[0][i], s);
+      } else {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) s = fma(c.S[2][l * NP + i], z[0][i], s);
+      }
+      rr(p)[l * NP + j] = s;
+    }
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
+    const int u = it * NT + tid;
+    if (u >= PB * NP) continue;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+    const int p = u / NP, i = u - (u / NP) * NP;
+    int64_t vx, vy;
+    if (!vert(p, vx, vy)) continue;
+    T z[NP];
+#pragma unroll
+    for (int l = 0; l < NP; ++l) z[l] = rr(p)[i * NP + l];
+    const int varx = variant_of(vx, N);
+    const int64_t row = ((vy - 1) * K + i) * n + (vx - 1) * K;
+#pragma unroll
+    for (int l = 0; l < NP; ++l) {
+      T s = 0;
+      if (varx == 1) {
+#pragma unroll
+        for (int m = 0; m < NP; ++m) s = fma(c.S[1][l * NP + m], z[m], s);
+      } else if (varx == 0) {
+#pragma unroll
+        for (int m = 0; m < NP; ++m) s = fma(c.S[0][l * NP + m], z[m], s);
+      } else {
+#pragma unroll
+        for (int m = 0; m < NP; ++m) s = fma(c.S[2][l * NP + m], z[m], s);
+      }
+      P.x[row + l] = fma(P.factor, s, P.x[row + l]);
+    }
   }
 }
 
@@ -724,11 +998,10 @@ static int persistent_grid(KernelT kern, size_t smem, int ntiles) {
 }
 
 template <typename T, int K>
-static void launch_apply(const FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st) {
+static void launch_apply(const FusedLevel& F, const T* x, const T* b, T* y, const SlabWindow& w, cudaStream_t st) {
   using LY = ApplyLayout<T, K>;
   const size_t smem = sizeof(T) * size_t(LY::TOTAL);
   static int grid_cache = -1;
-  const int ntx = int((F.N + LY::C - 1) / LY::C);
   if (grid_cache < 0) {
     cudaFuncSetAttribute(apply2d_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(apply2d_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -739,16 +1012,18 @@ static void launch_apply(const FusedLevel& F, const T* x, const T* b, T* y, cuda
   p.x = x; p.b = b; p.y = y; p.N = F.N; p.n = F.n;
   p.scale = T(1.0 / (F.h * F.h));
   p.zero = 0;
-  const int grid = std::min(grid_cache, ntx * ntx);
+  p.row0 = w.row0; p.lrows = w.lrows; p.out_lo = w.out_lo; p.out_hi = w.out_hi;
+  const int64_t ntx = (F.N + LY::C - 1) / LY::C;
+  const int64_t nty = ((w.out_hi - 1) / K) / LY::C - (w.out_lo / K) / LY::C + 1;
+  const int grid = (int)std::min<int64_t>(grid_cache, ntx * nty);
   apply2d_kernel<T, K><<<grid, 256, smem, st>>>(p);
 }
 
 template <typename T, int K>
-static void launch_fdm(const FusedLevel& F, T omega, const T* r, T* x, cudaStream_t st) {
+static void launch_fdm(const FusedLevel& F, T omega, const T* r, T* x, const SlabWindow& w, cudaStream_t st) {
   using LY = FdmLayout<T, K>;
   const size_t smem = sizeof(T) * size_t(LY::TOTAL);
   static int grid_cache = -1;
-  const int ntx = int((F.N + LY::C - 1) / LY::C);
   if (grid_cache < 0) {
     cudaFuncSetAttribute(fdm2d_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(fdm2d_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -759,55 +1034,115 @@ static void launch_fdm(const FusedLevel& F, T omega, const T* r, T* x, cudaStrea
   p.r = r; p.x = x; p.N = F.N; p.n = F.n;
   p.factor = T(double(omega) * F.h * F.h);
   p.zero = 0;
-  const int grid = std::min(grid_cache, ntx * ntx);
+  p.row0 = w.row0; p.lrows = w.lrows; p.out_lo = w.out_lo; p.out_hi = w.out_hi;
+  const int64_t ntx = (F.N + LY::C - 1) / LY::C;
+  const int64_t nty = ((w.out_hi - 1) / K) / LY::C - (w.out_lo / K) / LY::C + 1;
+  const int grid = (int)std::min<int64_t>(grid_cache, ntx * nty);
   fdm2d_kernel<T, K><<<grid, 256, smem, st>>>(p);
 }
 
+static SlabWindow full_window(const FusedLevel& F) { return SlabWindow{0, F.n, 1, int64_t(F.k) * F.N}; }
+
+static void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
 template <typename T>
-bool fused_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches) {
+bool fused_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches,
+                 const SlabWindow* win) {
   if (F.d != 2) return false;
+  const SlabWindow w = win ? *win : full_window(F);
+  if (w.out_hi <= w.out_lo) return true;
   switch (F.k) {
-    case 2: launch_apply<T, 2>(F, x, b, y, st); break;
-    case 3: launch_apply<T, 3>(F, x, b, y, st); break;
-    case 4: launch_apply<T, 4>(F, x, b, y, st); break;
-    case 5: launch_apply<T, 5>(F, x, b, y, st); break;
-    case 6: launch_apply<T, 6>(F, x, b, y, st); break;
-    case 7: launch_apply<T, 7>(F, x, b, y, st); break;
+    case 2: launch_apply<T, 2>(F, x, b, y, w, st); break;
+    case 3: launch_apply<T, 3>(F, x, b, y, w, st); break;
+    case 4: launch_apply<T, 4>(F, x, b, y, w, st); break;
+    case 5: launch_apply<T, 5>(F, x, b, y, w, st); break;
+    case 6: launch_apply<T, 6>(F, x, b, y, w, st); break;
+    case 7: launch_apply<T, 7>(F, x, b, y, w, st); break;
     default: return false;
   }
   (*launches)++;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) throw std::runtime_error(std::string("fused apply2d launch: ") + cudaGetErrorString(e));
+  check_launch("fused apply2d launch");
+  return true;
+}
+
+template <typename T>
+bool fused_fdm(FusedLevel& F, T omega, const T* r, T* x, cudaStream_t st, int64_t* launches, const SlabWindow* win) {
+  if (F.d != 2) return false;
+  const SlabWindow w = win ? *win : full_window(F);
+  if (w.out_hi <= w.out_lo) return true;
+  switch (F.k) {
+    case 2: launch_fdm<T, 2>(F, omega, r, x, w, st); break;
+    case 3: launch_fdm<T, 3>(F, omega, r, x, w, st); break;
+    case 4: launch_fdm<T, 4>(F, omega, r, x, w, st); break;
+    case 5: launch_fdm<T, 5>(F, omega, r, x, w, st); break;
+    case 6: launch_fdm<T, 6>(F, omega, r, x, w, st); break;
+    case 7: launch_fdm<T, 7>(F, omega, r, x, w, st); break;
+    default: return false;
+  }
+  (*launches)++;
+  check_launch("fused fdm2d launch");
   return true;
 }
 
 template <typename T>
 bool fused_avs(FusedLevel& F, T omega, const T* b, T* x, T* scratch, cudaStream_t st, int64_t* launches) {
   if (F.d != 2) return false;
-  fused_apply<T>(F, x, b, scratch, st, launches);             // r = b - A x (one residual per step)
-  switch (F.k) {
-    case 2: launch_fdm<T, 2>(F, omega, scratch, x, st); break;
-    case 3: launch_fdm<T, 3>(F, omega, scratch, x, st); break;
-    case 4: launch_fdm<T, 4>(F, omega, scratch, x, st); break;
-    case 5: launch_fdm<T, 5>(F, omega, scratch, x, st); break;
-    case 6: launch_fdm<T, 6>(F, omega, scratch, x, st); break;
-    case 7: launch_fdm<T, 7>(F, omega, scratch, x, st); break;
-    default: return false;
+  fused_apply<T>(F, x, b, scratch, st, launches, nullptr);       // r = b - A x (one residual per step)
+  return fused_fdm<T>(F, omega, scratch, x, st, launches, nullptr);
+}
+
+template <typename T, int K>
+static void launch_mvs(const FusedLevel& F, const int32_t* list, int64_t count, T omega, const T* b, T* x,
+                       cudaStream_t st) {
+  using LY = MvsLayout<T, K>;
+  const size_t smem = sizeof(T) * size_t(LY::TOTAL);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(mvs2d_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(mvs2d_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr = true;
   }
-  (*launches)++;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) throw std::runtime_error(std::string("fused fdm2d launch: ") + cudaGetErrorString(e));
-  return true;
+  MvsP<T, K> p;
+  std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
+  p.x = x; p.b = b; p.list = list; p.count = count; p.N = F.N; p.n = F.n;
+  p.scale = T(1.0 / (F.h * F.h));
+  p.factor = T(double(omega) * F.h * F.h);
+  p.zero = 0;
+  const int64_t grid = (count + LY::PB - 1) / LY::PB;
+  mvs2d_kernel<T, K><<<(unsigned)grid, 256, smem, st>>>(p);
 }
 
 template <typename T>
-bool fused_mvs_color(FusedLevel&, int, T, const T*, T*, cudaStream_t, int64_t*) { return false; }
+bool fused_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega, const T* b, T* x, cudaStream_t st,
+                     int64_t* launches) {
+  if (F.d != 2) return false;
+  if (count == 0) return true;
+  switch (F.k) {
+    case 2: launch_mvs<T, 2>(F, list, count, omega, b, x, st); break;
+    case 3: launch_mvs<T, 3>(F, list, count, omega, b, x, st); break;
+    case 4: launch_mvs<T, 4>(F, list, count, omega, b, x, st); break;
+    case 5: launch_mvs<T, 5>(F, list, count, omega, b, x, st); break;
+    case 6: launch_mvs<T, 6>(F, list, count, omega, b, x, st); break;
+    case 7: launch_mvs<T, 7>(F, list, count, omega, b, x, st); break;
+    default: return false;
+  }
+  (*launches)++;
+  check_launch("fused mvs2d launch");
+  return true;
+}
 
-template bool fused_apply<double>(FusedLevel&, const double*, const double*, double*, cudaStream_t, int64_t*);
-template bool fused_apply<float>(FusedLevel&, const float*, const float*, float*, cudaStream_t, int64_t*);
-template bool fused_avs<double>(FusedLevel&, double, const double*, double*, double*, cudaStream_t, int64_t*);
-template bool fused_avs<float>(FusedLevel&, float, const float*, float*, float*, cudaStream_t, int64_t*);
-template bool fused_mvs_color<double>(FusedLevel&, int, double, const double*, double*, cudaStream_t, int64_t*);
-template bool fused_mvs_color<float>(FusedLevel&, int, float, const float*, float*, cudaStream_t, int64_t*);
+bool fused_supports_slab(const FusedLevel& F) { return F.d == 2; }
+
+#define C0IP_INST(T)                                                                                       \
+  template bool fused_apply<T>(FusedLevel&, const T*, const T*, T*, cudaStream_t, int64_t*, const SlabWindow*); \
+  template bool fused_fdm<T>(FusedLevel&, T, const T*, T*, cudaStream_t, int64_t*, const SlabWindow*);        \
+  template bool fused_avs<T>(FusedLevel&, T, const T*, T*, T*, cudaStream_t, int64_t*);                        \
+  template bool fused_mvs_color<T>(FusedLevel&, const int32_t*, int64_t, T, const T*, T*, cudaStream_t, int64_t*);
+C0IP_INST(double)
+C0IP_INST(float)
+#undef C0IP_INST
 
 }  // namespace c0ip

@@ -263,3 +263,47 @@ def test_bad_level_is_arg_error():
     with pytest.raises(_lib.C0ipError) as e:
         ctx.apply(L + 1, torch.zeros(10, device=DEV, dtype=torch.float64))
     assert e.value.status == _lib.ERR_ARG
+
+
+# ------------------------------------------------------------------------------ slabs (multi-GPU path)
+@pytest.mark.parametrize("k,N,R", [(2, 32, 2), (4, 16, 2), (3, 20, 3), (7, 12, 2)])
+def test_slab_step_bitwise_equals_single_domain(k, N, R):
+    """Each rank's slab step (window with exchanged ghosts) == the single-domain step on its owned rows
+    (same tiles, same arithmetic -> bitwise); apply likewise.  Ranks are emulated on one GPU."""
+    from paper_2412_05082_b200 import api
+    from paper_2412_05082_b200.dist import partition
+    ctx = api.Context(2, k, 3, cells_override=N)
+    L = 3
+    n = k * N - 1
+    x, b = random_xb(k, 2, N)
+    full = torch.tensor(x, device=DEV)
+    ctx.smooth(L, "avs", 1, 0.25, torch.tensor(b, device=DEV), full)
+    yfull = ctx.apply(L, torch.tensor(x, device=DEV))
+    ga, gp = ctx.slab_ghosts()
+    assert ga == 4 * k - 2 and gp == 2 * k
+    out = torch.empty_like(full)
+    yout = torch.empty_like(full)
+    for s in partition(N, k, R, ga):
+        rows = slice(s.win_lo - 1, s.win_hi - 1)
+        xw = torch.tensor(x.reshape(n, n)[rows].ravel(), device=DEV)
+        bw = torch.tensor(b.reshape(n, n)[rows].ravel(), device=DEV)
+        rw = torch.empty_like(xw)
+        ctx.slab_avs_step(L, 0.25, s.row0, s.lrows, s.own_lo, s.own_hi, bw, xw, rw)
+        out.view(n, n)[s.own_lo - 1:s.own_hi - 1] = xw.view(-1, n)[s.own_local]
+        yw = torch.empty_like(xw)
+        ctx.slab_apply(L, s.row0, s.lrows, s.own_lo, s.own_hi, torch.tensor(x.reshape(n, n)[rows].ravel(), device=DEV), yw)
+        yout.view(n, n)[s.own_lo - 1:s.own_hi - 1] = yw.view(-1, n)[s.own_local]
+    assert torch.equal(out, full)
+    assert torch.equal(yout, yfull)
+    ctx.close()
+
+
+def test_slab_rejects_missing_ghosts():
+    from paper_2412_05082_b200 import api, _lib
+    ctx = api.Context(2, 3, 3, cells_override=16)
+    n = 3 * 16 - 1
+    xw = torch.zeros(10 * n, device=DEV, dtype=torch.float64)
+    with pytest.raises(_lib.C0ipError) as e:
+        ctx.slab_avs_step(3, 0.25, 10, 10, 12, 18, xw, xw.clone(), xw.clone())
+    assert e.value.status == _lib.ERR_ARG
+    ctx.close()
