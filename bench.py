@@ -30,7 +30,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from c0ip_inputs import CFG2_CELLS, random_xb  # noqa: E402
+from c0ip_inputs import CFG2_CELLS, CFG4_CELLS, random_xb  # noqa: E402
 
 METRIC = "smoother & C0IP matvec GDoF/s; MG-PCG time-to-solve, FP64 vs mixed precision"
 
@@ -59,6 +59,16 @@ def flops_residual_2d(k):
     # x-stage B^ (avg 3k+2 nonzeros), L^, M^ (avg k+2) and the same on the y-stage, 2 flop/MAC
     per = (3 * k + 2) + 2 * (k + 2)
     return 2.0 * 2 * per
+
+
+def flops_residual_3d(k):
+    # x-stage (B, L, M), y-stage (6 contractions), z-stage (3): MACs with banded averages 3k+2 / k+2
+    return 2.0 * ((3 * k + 2) + 2 * (k + 2) + (3 * k + 2) + 5 * (k + 2) + (3 * k + 2) + 2 * (k + 2))
+
+
+def flops_fdm_3d(k):
+    np_ = 2 * k - 1
+    return 2.0 * 6 * np_ ** 4 / k ** 3
 
 
 def flops_fdm_2d(k):
@@ -292,6 +302,7 @@ def main():
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--dim", type=int, default=2, choices=[2, 3])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -305,17 +316,18 @@ def main():
     k = args.degree
     if world > 1:
         return run_slabs(args, world, rank, local)
-    N = CFG2_CELLS[k]
+    d = args.dim
+    N = CFG2_CELLS[k] if d == 2 else CFG4_CELLS[k]
     dt = torch.float64 if args.dtype == "f64" else torch.float32
-    ctx = api.Context(2, k, 3, cells_override=N, device=local)
+    ctx = api.Context(d, k, 3, cells_override=N, device=local)
     L = 3
     ndofs = ctx.n_dofs(L)
-    x0, b0 = random_xb(k, 2, N)
+    x0, b0 = random_xb(k, d, N)
     x = torch.tensor(x0, device="cuda", dtype=dt)
     b = torch.tensor(b0, device="cuda", dtype=dt)
     r = torch.empty_like(x)
     stream = torch.cuda.current_stream()
-    omega = 0.25
+    omega = 0.25 if d == 2 else 0.1
 
     def step():
         ctx.smooth(L, "avs", 1, omega, b, x)
@@ -351,6 +363,17 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         t_mv_ms = e0.elapsed_time(e1) / args.steps
+        # one coloured multiplicative step (8 colours, residual per colour), omega = 1
+        xm = x.clone()
+        om_m = 1.0 if d == 2 else 0.7
+        ctx.smooth(L, "mvs", 1, om_m, b, xm)
+        mreps = max(2, args.steps // 4)
+        e0.record(stream)
+        for _ in range(mreps):
+            ctx.smooth(L, "mvs", 1, om_m, b, xm)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_mvs_ms = e0.elapsed_time(e1) / mreps
     barrier(world)
     t_step_ms = max_over_ranks(t_step_ms, world)
     clocks = clk.summary()
@@ -383,9 +406,13 @@ def main():
     clk_mhz = clocks.get("sm_mhz") or mhz
     t_fdm_ms = max(t_step_ms - t_res_ms, 1e-9)
     # dominant kernel of the step and its roofline (algorithmic work / live CUDA-event time)
-    kern = "fdm2d" if t_fdm_ms >= t_res_ms else "apply2d"
-    t_k = t_fdm_ms if kern == "fdm2d" else t_res_ms
-    flop = (flops_fdm_2d(k) if kern == "fdm2d" else flops_residual_2d(k)) * ndofs
+    if d == 2:
+        kern = "fdm2d" if t_fdm_ms >= t_res_ms else "apply2d"
+        flop = (flops_fdm_2d(k) if kern == "fdm2d" else flops_residual_2d(k)) * ndofs
+    else:
+        kern = "patch_fdm3d" if t_fdm_ms >= t_res_ms else "apply3d"
+        flop = (flops_fdm_3d(k) if kern == "patch_fdm3d" else flops_residual_3d(k)) * ndofs
+    t_k = t_fdm_ms if kern in ("fdm2d", "patch_fdm3d") else t_res_ms
     byts = 3 * esz * ndofs
     peak_alu = fp64_peak_tflops(clk_mhz) if esz == 8 else fp32_peak_tflops(clk_mhz)
     ach_tf = flop / (t_k * 1e-3) / 1e12
@@ -410,8 +437,10 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_step_ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": f"cfg2: 2D unit square, Q{k} C0IP, N={N} cells/axis ({ndofs} DoFs), one additive "
-                               f"vertex-patch smoothing step (atomic-free gather AVS, omega=1/4)",
+        "config": {"workload": (f"cfg2: 2D unit square, Q{k} C0IP, N={N} cells/axis ({ndofs} DoFs), one additive "
+                                f"vertex-patch smoothing step (atomic-free gather AVS, omega=1/4)") if d == 2 else
+                               (f"cfg4: 3D unit cube, Q{k} C0IP, N={N} cells/axis ({ndofs} DoFs), one additive "
+                                f"vertex-patch smoothing step (parity-coloured AVS, omega=0.1)"),
                    "degree": k, "cells": N, "dofs_per_gpu": ndofs,
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "inputs larger than L2 (x, b, r = 3 x %.0f MB)" % (ndofs * esz / 1e6)},
@@ -422,32 +451,35 @@ def main():
         "roofline": roof,
         "matvec": {"value": round(ndofs * world / (t_mv_ms * 1e-3) / 1e9, 3), "unit": "GDoF/s",
                    "ms": round(t_mv_ms, 4)},
+        "mvs": {"value": round(ndofs * world / (t_mvs_ms * 1e-3) / 1e9, 3), "unit": "GDoF/s",
+                "ms": round(t_mvs_ms, 4), "note": "one coloured MVS step, 8 colours, omega=1"},
         "residual_ms": round(t_res_ms, 4), "fdm_ms": round(t_fdm_ms, 4),
     }
 
     if not args.no_pcg:
         # MG-PCG time-to-solve on the nested mesh N = 2^L of similar size
-        Lp = {2: 11, 3: 10, 4: 10, 5: 9, 6: 9, 7: 9}[k]
+        Lp = ({2: 11, 3: 10, 4: 10, 5: 9, 6: 9, 7: 9} if d == 2 else {2: 7, 3: 7, 4: 6, 5: 6})[k]
         ctx.close()
-        cp = api.Context(2, k, Lp, device=local)
+        cp = api.Context(d, k, Lp, device=local)
         bb = cp.rhs(Lp)
         res = {}
         for name, cdt in (("fp64", torch.float64), ("mixed", torch.float32)):
-            mg = api.MG("avs", 2, 0.25, cycle_dtype=cdt)
+            mg = api.MG("avs", 2, 0.25 if d == 2 else 0.1, cycle_dtype=cdt)
             cp.pcg(mg, bb, max_iter=3)            # warm-up (allocations, first launches)
             torch.cuda.synchronize()
             xs, rep, hist = cp.pcg(mg, bb)
             res[name] = {"seconds": round(rep["seconds"], 4), "iterations": rep["iterations"],
                          "nu": round(rep["nu"], 2), "converged": rep["converged"]}
         res["dofs"] = cp.n_dofs(Lp)
-        res["config"] = f"2D Q{k}, L={Lp} (N={2 ** Lp}), AVS 2+2 steps omega=1/4, CG rtol 1e-8, x0=0, paper load"
+        res["config"] = (f"{d}D Q{k}, L={Lp} (N={2 ** Lp}), AVS 2+2 steps omega={0.25 if d == 2 else 0.1}, "
+                         f"CG rtol 1e-8, x0=0, paper load")
         res["mixed_speedup"] = round(res["fp64"]["seconds"] / res["mixed"]["seconds"], 3)
         line["pcg"] = res
         cp.close()
     else:
         ctx.close()
 
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and d == 2:
         line["cpu_baseline"] = cpu_oracle_sample(k)
     if rank == 0:
         print(json.dumps(line))

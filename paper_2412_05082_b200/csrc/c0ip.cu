@@ -264,9 +264,10 @@ void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStr
 
 template <typename T>
 void apply_op(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStream_t st) {
-  if (ctx->path == C0IP_PATH_AUTO && L.fused &&
-      c0ip::fused_apply<T>(*L.fused, x, b, y, st, &ctx->launches))
-    return;
+  if (ctx->path == C0IP_PATH_AUTO && L.fused) {
+    if (c0ip::fused_dim(*L.fused) == 2 && c0ip::fused_apply<T>(*L.fused, x, b, y, st, &ctx->launches)) return;
+    if (c0ip::fused_dim(*L.fused) == 3 && c0ip::fused3_apply<T>(*L.fused, x, b, y, st, &ctx->launches)) return;
+  }
   generic_apply<T>(ctx, L, x, b, y, st);
 }
 
@@ -293,6 +294,16 @@ void patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, const int32_
   CK(cudaGetLastError());
 }
 
+// x += omega A~_v^{-1} R_v r over disjoint patches (tuned 3D kernel when available, else generic)
+template <typename T>
+void disjoint_patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, const int32_t* list, int64_t count,
+                          cudaStream_t st) {
+  if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
+      c0ip::fused3_patch_fdm<T>(*L.fused, omega, r, x, list, count, st, &ctx->launches))
+    return;
+  patch_solve<T>(ctx, L, r, x, omega, list, count, 0, st);
+}
+
 template <typename T>
 void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, bool reverse,
                  const T* b, T* x, cudaStream_t st) {
@@ -311,7 +322,7 @@ void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, b
                                      &ctx->launches))
           continue;
         apply_op<T>(ctx, L, x, b, t.sres.p, st);                 // residual per colour
-        patch_solve<T>(ctx, L, t.sres.p, x, omega, L.colors_d.p + L.color_off[c], cnt, 0, st);
+        disjoint_patch_solve<T>(ctx, L, t.sres.p, x, omega, L.colors_d.p + L.color_off[c], cnt, st);
       }
       continue;
     }
@@ -324,7 +335,7 @@ void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, b
     } else {   // coloured / deterministic generic: serialise writes over the 2^d parity classes
       for (int c = 0; c < (1 << d); ++c) {
         int64_t cnt = L.parity_off[c + 1] - L.parity_off[c];
-        patch_solve<T>(ctx, L, t.sres.p, x, omega, L.parity_d.p + L.parity_off[c], cnt, 0, st);
+        disjoint_patch_solve<T>(ctx, L, t.sres.p, x, omega, L.parity_d.p + L.parity_off[c], cnt, st);
       }
     }
   }

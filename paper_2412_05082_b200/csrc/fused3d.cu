@@ -1,0 +1,454 @@
+// Fused kernels for large 3D levels (sm_100a, FP64 and FP32), k = 2..5.
+//
+//   apply3d      : r = b - A x (or y = A x) with A = h^-1 (B^M^M^ + M^B^M^ + M^M^B^ + 2(L^L^M^ + M^L^L^ +
+//                  L^M^L^)) (Eq. c0iptensorvp3D).  A CTA owns a C x C in-plane tile
+//                  and a chunk of CZ cell layers along z and streams through z: per cell layer it
+//                  builds, for K new node planes, the in-plane results
+//                    P = B^_y M^_x + M^_y B^_x + 2 L^_y L^_x,  Q = L^_y M^_x + M^_y L^_x,  R = M^_y M^_x
+//                  (x- and y-stages in shared memory) and each thread, owning one in-plane node, keeps
+//                  sliding register windows of P, Q, R along z and emits
+//                    y = M^_z P + 2 L^_z Q + B^_z R
+//                  for the finished cell layer (output-centric banded rows, uniform coefficients).
+//   patch_fdm3d  : x += omega h A~_v^{-1} R_v r for a list of patches: per patch the
+//                  six 1D contractions (S^T along x, y, z; divide by lambda_x + lambda_y + lambda_z; S
+//                  along z, y, x) with one thread per patch line and register-blocked lines.  Launched
+//                  per parity class (2^d non-overlapping classes, plain stores: deterministic) for the
+//                  additive smoother and per colour for the multiplicative one.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "fused_common.cuh"
+
+namespace c0ip {
+
+template <int K>
+struct Tile3 {
+  static constexpr int C = (K == 2) ? 8 : (K == 3) ? 5 : (K == 4) ? 4 : 3;   // in-plane cells
+  static constexpr int O = C * K;                                            // owned nodes per axis (<= 16)
+  static constexpr int CZ = 32;                                              // cell layers per chunk
+};
+
+template <typename T, int K>
+struct Apply3P {
+  Coef2<T, K> c;
+  const T* x;
+  const T* b;
+  T* y;
+  int64_t N, n;
+  T scale;                  // h^-1
+  int zero;
+};
+
+template <typename T, int K>
+struct Apply3Layout {
+  static constexpr int C = Tile3<K>::C, O = Tile3<K>::O;
+  static constexpr int BW = (C + 3) * K + 1;      // in-plane box [(c0-2)K, (c0+C+1)K]
+  static constexpr int PX = odd(BW), PO = odd(O);
+  static constexpr int XB = K * BW * PX;          // K planes of the box
+  static constexpr int SX = K * 3 * BW * PO;      // x-stage outputs (B, L, M) of K planes
+  static constexpr int PQR = K * 3 * O * O;       // in-plane results of K planes
+  static constexpr int TOTAL = XB + SX + PQR;
+};
+
+// banded row of class PP applied to a window w (w index o <-> offset o - 2K around the output node)
+template <typename T, int K, int PP, int W, typename F>
+__device__ __forceinline__ T row_band(F coef, const T* w, int base) {
+  T s = 0;
+#pragma unroll
+  for (int q = 0; q <= W - 1; ++q) {
+    const bool nz = (W == 4 * K + 1) ? (PP == 0 || (q >= K - PP && q <= 4 * K - PP))
+                                     : (PP == 0 || (q >= K - PP && q <= 2 * K - PP));
+    if (nz) s = fma(coef(q), w[base + PP + q], s);
+  }
+  return s;
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(256, 1) apply3d_kernel(const __grid_constant__ Apply3P<T, K> P) {
+  using LY = Apply3Layout<T, K>;
+  constexpr int C = LY::C, O = LY::O, BW = LY::BW, PX = LY::PX, PO = LY::PO, CZ = Tile3<K>::CZ;
+  constexpr int NT = 256;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+  T* xb = sm;                     // [K][BW][PX]
+  T* sx = xb + LY::XB;            // [K][3][BW][PO]  (0: B^x, 1: L^x, 2: M^x)
+  T* pqr = sx + LY::SX;           // [K][3][O][O]    (0: P, 1: Q, 2: R)
+  const int64_t N = P.N, n = P.n, KN = K * N;
+  const int ntx = int((N + C - 1) / C);
+  const int tile = blockIdx.x % (ntx * ntx), chunk = blockIdx.x / (ntx * ntx);
+  const int64_t cx0 = int64_t(tile % ntx) * C, cy0 = int64_t(tile / ntx) * C, cz0 = int64_t(chunk) * CZ;
+  const int tid = threadIdx.x;
+  const int oy = tid / O, ox = tid - (tid / O) * O;       // z-stage ownership (tid < O*O)
+  const bool zown = tid < O * O;
+  T wR[4 * K + 1], wP[3 * K + 1], wQ[3 * K + 1];
+#pragma unroll
+  for (int i = 0; i <= 4 * K; ++i) wR[i] = 0;
+#pragma unroll
+  for (int i = 0; i <= 3 * K; ++i) wP[i] = wQ[i] = 0;
+  int round = 0;
+  const int nsteps = int(std::min<int64_t>(CZ, N - cz0)) + 4;
+
+  for (int s = 0; s < nsteps; ++s) {
+    // node planes of this step: zp = (cz0 - 3 + s) K + 1 + pz, pz < K
+    const int64_t z0 = (cz0 - 3 + s) * K + 1;
+    for (int e = tid; e < K * BW * BW; e += NT) {
+      const int pz = e / (BW * BW), rem = e - pz * (BW * BW), r = rem / BW, cc = rem - (rem / BW) * BW;
+      const int64_t jz = z0 + pz, jy = (cy0 - 2) * K + r, jx = (cx0 - 2) * K + cc;
+      T v = 0;
+      if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1 && jz >= 1 && jz <= KN - 1)
+        v = P.x[((jz - 1) * n + (jy - 1)) * n + (jx - 1)];
+      xb[(pz * BW + r) * PX + cc] = v;
+    }
+    __syncthreads();
+
+    // x-stage: unit = (plane, box row, cell) -> B^ L^ M^ along x for the K nodes of the cell
+#pragma unroll 1
+    for (int it = 0; it < cdiv(K * BW * C, NT); ++it, ++round) {
+      const int u = it * NT + tid;
+      if (u >= K * BW * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      const int r = u % BW, rest = u / BW, ci = rest % C, pz = rest / C;
+      const int64_t cx = cx0 + ci;
+      if (cx >= N) continue;
+      T w[1][4 * K + 1];
+#pragma unroll
+      for (int q = 0; q <= 4 * K; ++q) w[0][q] = xb[(pz * BW + r) * PX + ci * K + q];
+      const bool inner = (cx >= 2 && cx <= N - 2);
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        T ob[1] = {0}, ol[1] = {0}, om[1] = {0};
+        const int sp = inner ? -1 : special_row<K>(cx * K + p, N);
+        with_p<K>(p, [&](auto PC) {
+          constexpr int PP = decltype(PC)::value;
+          if (sp < 0) {
+            rowB<T, K, PP>([&](int q) { return c.BI[PP][q]; }, w, 0, ob);
+            rowML<T, K, PP>([&](int q) { return c.LI[PP][q]; }, w, K, ol);
+            rowML<T, K, PP>([&](int q) { return c.MI[PP][q]; }, w, K, om);
+          } else {
+            rowB<T, K, PP>([&](int q) { return c.BS[sp][q]; }, w, 0, ob);
+            rowML<T, K, PP>([&](int q) { return c.LS[sp][q + K]; }, w, K, ol);
+            rowML<T, K, PP>([&](int q) { return c.MS[sp][q + K]; }, w, K, om);
+          }
+        });
+        sx[((pz * 3 + 0) * BW + r) * PO + ci * K + p] = ob[0];
+        sx[((pz * 3 + 1) * BW + r) * PO + ci * K + p] = ol[0];
+        sx[((pz * 3 + 2) * BW + r) * PO + ci * K + p] = om[0];
+      }
+    }
+    __syncthreads();
+
+    // y-stage: unit = (plane, owned column, cell row) -> P, Q, R for the K nodes of the cell row
+#pragma unroll 1
+    for (int it = 0; it < cdiv(K * O * C, NT); ++it, ++round) {
+      const int u = it * NT + tid;
+      if (u >= K * O * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      const int col = u % O, rest = u / O, ci = rest % C, pz = rest / C;
+      const int64_t cy = cy0 + ci;
+      if (cy >= N) continue;
+      const T* sB = sx + (pz * 3 + 0) * BW * PO;
+      const T* sL = sx + (pz * 3 + 1) * BW * PO;
+      const T* sM = sx + (pz * 3 + 2) * BW * PO;
+      T wM[4 * K + 1], wB[2 * K + 1], wL[2 * K + 1];
+#pragma unroll
+      for (int q = 0; q <= 4 * K; ++q) wM[q] = sM[(ci * K + q) * PO + col];
+#pragma unroll
+      for (int q = 0; q <= 2 * K; ++q) {
+        wB[q] = sB[(ci * K + K + q) * PO + col];
+        wL[q] = sL[(ci * K + K + q) * PO + col];
+      }
+      const bool inner = (cy >= 2 && cy <= N - 2);
+#pragma unroll
+      for (int p = 0; p < K; ++p) {
+        const int sp = inner ? -1 : special_row<K>(cy * K + p, N);
+        T vP = 0, vQ = 0, vR = 0;
+        with_p<K>(p, [&](auto PC) {
+          constexpr int PP = decltype(PC)::value;
+          if (sp < 0) {
+            vP = row_band<T, K, PP, 4 * K + 1>([&](int q) { return c.BI[PP][q]; }, wM, 0) +
+                 row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MI[PP][q]; }, wB, 0) +
+                 T(2) * row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LI[PP][q]; }, wL, 0);
+            vQ = row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LI[PP][q]; }, wM, K) +
+                 row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MI[PP][q]; }, wL, 0);
+            vR = row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MI[PP][q]; }, wM, K);
+          } else {
+            vP = row_band<T, K, PP, 4 * K + 1>([&](int q) { return c.BS[sp][q]; }, wM, 0) +
+                 row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MS[sp][q + K]; }, wB, 0) +
+                 T(2) * row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LS[sp][q + K]; }, wL, 0);
+            vQ = row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LS[sp][q + K]; }, wM, K) +
+                 row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MS[sp][q + K]; }, wL, 0);
+            vR = row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MS[sp][q + K]; }, wM, K);
+          }
+        });
+        const int orow = ci * K + p;
+        pqr[((pz * 3 + 0) * O + orow) * O + col] = vP;
+        pqr[((pz * 3 + 1) * O + orow) * O + col] = vQ;
+        pqr[((pz * 3 + 2) * O + orow) * O + col] = vR;
+      }
+    }
+    __syncthreads();
+
+    // z-stage: shift the windows by K planes, append the new ones, emit the finished cell layer
+    if (zown) {
+#pragma unroll
+      for (int i = 0; i <= 3 * K; ++i) wR[i] = wR[i + K];
+#pragma unroll
+      for (int i = 0; i <= 2 * K; ++i) { wP[i] = wP[i + K]; wQ[i] = wQ[i + K]; }
+#pragma unroll
+      for (int pz = 0; pz < K; ++pz) {
+        wP[2 * K + 1 + pz] = pqr[((pz * 3 + 0) * O + oy) * O + ox];
+        wQ[2 * K + 1 + pz] = pqr[((pz * 3 + 1) * O + oy) * O + ox];
+        wR[3 * K + 1 + pz] = pqr[((pz * 3 + 2) * O + oy) * O + ox];
+      }
+    }
+    // after this step the newest plane is (cz0 - 2 + s) K: layer cz = cz0 + s - 4 is complete
+    const int64_t cz = cz0 + s - 4;
+    if (s >= 4 && zown) {
+      const int64_t jx = cx0 * K + ox, jy = cy0 * K + oy;
+      if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1) {
+        const Coef2<T, K>& c = coef_at(P.c, (round++) * P.zero);
+        const bool inner = (cz >= 2 && cz <= N - 2);
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const int64_t jz = cz * K + p;
+          if (jz < 1 || jz > KN - 1) continue;
+          const int sp = inner ? -1 : special_row<K>(jz, N);
+          T v = 0;
+          // windows: wR[i] <-> plane (cz-2)K + i ; wP/wQ[i] <-> plane (cz-1)K + i
+          with_p<K>(p, [&](auto PC) {
+            constexpr int PP = decltype(PC)::value;
+            if (sp < 0)
+              v = row_band<T, K, PP, 4 * K + 1>([&](int q) { return c.BI[PP][q]; }, wR, 0) +
+                  row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MI[PP][q]; }, wP, 0) +
+                  T(2) * row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LI[PP][q]; }, wQ, 0);
+            else
+              v = row_band<T, K, PP, 4 * K + 1>([&](int q) { return c.BS[sp][q]; }, wR, 0) +
+                  row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MS[sp][q + K]; }, wP, 0) +
+                  T(2) * row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LS[sp][q + K]; }, wQ, 0);
+          });
+          const int64_t g = ((jz - 1) * n + (jy - 1)) * n + (jx - 1);
+          v *= P.scale;
+          P.y[g] = P.b ? P.b[g] - v : v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------------- patch_fdm3d
+template <typename T, int K>
+struct Fdm3P {
+  Coef2<T, K> c;
+  const T* r;
+  T* x;
+  const int32_t* list;      // patch ids (nullptr: 0..count-1)
+  int64_t count;
+  int64_t N, n;
+  T factor;                 // omega h (A~^-1 = h A^~^-1 in 3D)
+  int zero;
+};
+
+template <typename T, int K>
+struct Fdm3Layout {
+  static constexpr int NP = 2 * K - 1, NL = NP * NP * NP;
+  static constexpr int PB = cdiv(256, NP * NP);   // patches per CTA so that one stage ~ 256 lines
+  static constexpr int TOTAL = 2 * PB * NL;
+};
+
+// one 1D contraction along axis AX of every patch line: out = S^T in (TR) or S in (!TR)
+template <typename T, int K, int AX, bool TR>
+__device__ __forceinline__ void contract3(const Coef2<T, K>& c, int var, const T* in, T* out) {
+  constexpr int NP = 2 * K - 1;
+  constexpr int ST = AX == 0 ? 1 : (AX == 1 ? NP : NP * NP);
+  T w[NP];
+#pragma unroll
+  for (int l = 0; l < NP; ++l) w[l] = in[l * ST];
+  auto body = [&](auto VC) {
+    constexpr int V = decltype(VC)::value;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      T s = 0;
+#pragma unroll
+      for (int l = 0; l < NP; ++l) s = fma(TR ? c.S[V][l * NP + i] : c.S[V][i * NP + l], w[l], s);
+      out[i * ST] = s;
+    }
+  };
+  if (var == 1) body(std::integral_constant<int, 1>{});
+  else if (var == 0) body(std::integral_constant<int, 0>{});
+  else body(std::integral_constant<int, 2>{});
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_constant__ Fdm3P<T, K> P) {
+  using LY = Fdm3Layout<T, K>;
+  constexpr int NP = LY::NP, NL = LY::NL, PB = LY::PB;
+  constexpr int NT = 256;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* buf0 = reinterpret_cast<T*>(smem_raw);
+  T* buf1 = buf0 + PB * NL;
+  const int64_t N = P.N, n = P.n;
+  const int64_t first = (int64_t)blockIdx.x * PB;
+  const int tid = threadIdx.x;
+  int round = 0;
+  auto vert = [&](int p, int64_t* v) -> bool {
+    const int64_t q = first + p;
+    if (q >= P.count) return false;
+    const int64_t pid = P.list ? P.list[q] : q;
+    v[0] = 1 + pid % (N - 1);
+    v[1] = 1 + (pid / (N - 1)) % (N - 1);
+    v[2] = 1 + pid / ((N - 1) * (N - 1));
+    return true;
+  };
+  // gather R_v r
+  for (int e = tid; e < PB * NL; e += NT) {
+    const int p = e / NL, l = e - p * NL;
+    int64_t v[3];
+    T val = 0;
+    if (vert(p, v)) {
+      const int lx = l % NP, ly = (l / NP) % NP, lz = l / (NP * NP);
+      val = P.r[(((v[2] - 1) * K + lz) * n + (v[1] - 1) * K + ly) * n + (v[0] - 1) * K + lx];
+    }
+    buf0[e] = val;
+  }
+  __syncthreads();
+  T* in = buf0;
+  T* out = buf1;
+  // S^T along x, y, z; divide; S along z, y, x  (lines: one per thread, units = (patch, line))
+#pragma unroll
+  for (int stage = 0; stage < 6; ++stage) {
+    const int ax = stage < 3 ? stage : 5 - stage;
+#pragma unroll 1
+    for (int it = 0; it < cdiv(PB * NP * NP, NT); ++it, ++round) {
+      const int u = it * NT + tid;
+      if (u >= PB * NP * NP) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      const int p = u / (NP * NP), li = u - p * (NP * NP);
+      int64_t v[3];
+      if (!vert(p, v)) continue;
+      const int var = variant_of(v[ax], N);
+      // line start: the two other local coordinates from li
+      int base;
+      if (ax == 0) base = li * NP;                                   // (ly, lz) = li
+      else if (ax == 1) base = (li / NP) * NP * NP + (li % NP);      // (lx, lz)
+      else base = li;                                                // (lx, ly)
+      T* o = out + p * NL + base;
+      const T* ii = in + p * NL + base;
+      if (ax == 0) { if (stage < 3) contract3<T, K, 0, true>(c, var, ii, o); else contract3<T, K, 0, false>(c, var, ii, o); }
+      else if (ax == 1) { if (stage < 3) contract3<T, K, 1, true>(c, var, ii, o); else contract3<T, K, 1, false>(c, var, ii, o); }
+      else { if (stage < 3) contract3<T, K, 2, true>(c, var, ii, o); else contract3<T, K, 2, false>(c, var, ii, o); }
+    }
+    __syncthreads();
+    T* t = in; in = out; out = t;
+    if (stage == 2) {
+      for (int e = tid; e < PB * NL; e += NT) {
+        const int p = e / NL, l = e - p * NL;
+        int64_t v[3];
+        if (!vert(p, v)) continue;
+        const int lx = l % NP, ly = (l / NP) % NP, lz = l / (NP * NP);
+        in[e] /= (P.c.lam[variant_of(v[0], N)][lx] + P.c.lam[variant_of(v[1], N)][ly] +
+                  P.c.lam[variant_of(v[2], N)][lz]);
+      }
+      __syncthreads();
+    }
+  }
+  // scatter: x += omega h u  (disjoint patches within one launch: plain read-modify-write)
+  for (int e = tid; e < PB * NL; e += NT) {
+    const int p = e / NL, l = e - p * NL;
+    int64_t v[3];
+    if (!vert(p, v)) continue;
+    const int lx = l % NP, ly = (l / NP) % NP, lz = l / (NP * NP);
+    const int64_t g = (((v[2] - 1) * K + lz) * n + (v[1] - 1) * K + ly) * n + (v[0] - 1) * K + lx;
+    P.x[g] = fma(P.factor, in[e], P.x[g]);
+  }
+}
+
+// ----------------------------------------------------------------------------- host side
+template <typename T, int K>
+static void launch_apply3(const FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st) {
+  using LY = Apply3Layout<T, K>;
+  const size_t smem = sizeof(T) * size_t(LY::TOTAL);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(apply3d_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(apply3d_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr = true;
+  }
+  Apply3P<T, K> p;
+  std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
+  p.x = x; p.b = b; p.y = y; p.N = F.N; p.n = F.n;
+  p.scale = T(1.0 / F.h);
+  p.zero = 0;
+  const int64_t ntx = (F.N + LY::C - 1) / LY::C, nch = (F.N + Tile3<K>::CZ - 1) / Tile3<K>::CZ;
+  apply3d_kernel<T, K><<<(unsigned)(ntx * ntx * nch), 256, smem, st>>>(p);
+}
+
+template <typename T, int K>
+static void launch_fdm3(const FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
+                        cudaStream_t st) {
+  using LY = Fdm3Layout<T, K>;
+  const size_t smem = sizeof(T) * size_t(LY::TOTAL);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(patch_fdm3d_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(patch_fdm3d_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr = true;
+  }
+  Fdm3P<T, K> p;
+  std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
+  p.r = r; p.x = x; p.list = list; p.count = count; p.N = F.N; p.n = F.n;
+  p.factor = T(double(omega) * F.h);
+  p.zero = 0;
+  const int64_t grid = (count + LY::PB - 1) / LY::PB;
+  patch_fdm3d_kernel<T, K><<<(unsigned)grid, 256, smem, st>>>(p);
+}
+
+static void check3(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename T>
+bool fused3_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches) {
+  if (F.d != 3) return false;
+  switch (F.k) {
+    case 2: launch_apply3<T, 2>(F, x, b, y, st); break;
+    case 3: launch_apply3<T, 3>(F, x, b, y, st); break;
+    case 4: launch_apply3<T, 4>(F, x, b, y, st); break;
+    case 5: launch_apply3<T, 5>(F, x, b, y, st); break;
+    default: return false;
+  }
+  (*launches)++;
+  check3("fused apply3d launch");
+  return true;
+}
+
+template <typename T>
+bool fused3_patch_fdm(FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
+                      cudaStream_t st, int64_t* launches) {
+  if (F.d != 3) return false;
+  if (count == 0) return true;
+  switch (F.k) {
+    case 2: launch_fdm3<T, 2>(F, omega, r, x, list, count, st); break;
+    case 3: launch_fdm3<T, 3>(F, omega, r, x, list, count, st); break;
+    case 4: launch_fdm3<T, 4>(F, omega, r, x, list, count, st); break;
+    case 5: launch_fdm3<T, 5>(F, omega, r, x, list, count, st); break;
+    default: return false;
+  }
+  (*launches)++;
+  check3("fused patch_fdm3d launch");
+  return true;
+}
+
+template bool fused3_apply<double>(FusedLevel&, const double*, const double*, double*, cudaStream_t, int64_t*);
+template bool fused3_apply<float>(FusedLevel&, const float*, const float*, float*, cudaStream_t, int64_t*);
+template bool fused3_patch_fdm<double>(FusedLevel&, double, const double*, double*, const int32_t*, int64_t,
+                                       cudaStream_t, int64_t*);
+template bool fused3_patch_fdm<float>(FusedLevel&, float, const float*, float*, const int32_t*, int64_t,
+                                      cudaStream_t, int64_t*);
+
+}  // namespace c0ip

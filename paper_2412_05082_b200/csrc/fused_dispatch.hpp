@@ -42,4 +42,13 @@ template <typename T>
 bool fused_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega, const T* b, T* x,
                      cudaStream_t st, int64_t* launches);
 
+// 3D (fused3d.cu): matvec / residual, and the per-patch FDM update x += omega A~_v^{-1} R_v r over a
+// list of mutually disjoint patches (a parity class or a colour)
+template <typename T>
+bool fused3_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches);
+template <typename T>
+bool fused3_patch_fdm(FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
+                      cudaStream_t st, int64_t* launches);
+int fused_dim(const FusedLevel& F);
+
 }  // namespace c0ip
