@@ -112,7 +112,14 @@ struct c0ip_ctx_s {
   int64_t launches = 0;
   DevArr<double> pcg_r, pcg_z, pcg_p, pcg_Ap, dot_part, dot_out;
   double* dot_host = nullptr;
+  // captured V-cycle (CUDA graph) for the PCG loop: key = mg config; replayed on the caller's stream
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t vc_exec = nullptr;
+  c0ip_mg_config vc_key{};
+  int64_t vc_nodes = 0;
   ~c0ip_ctx_s() {
+    if (vc_exec) cudaGraphExecDestroy(vc_exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     for (auto& L : levels) {
       for (auto* t : {&L.t64.M, &L.t64.L, &L.t64.B, &L.t64.E, &L.t64.Et, &L.t64.sres, &L.t64.vx,
                       &L.t64.vb, &L.t64.vr})
@@ -456,6 +463,41 @@ void vcycle_top(c0ip_ctx ctx, const c0ip_mg_config& mg, const double* r, double*
     vcycle_rec<float>(ctx, ctx->lmax, mg, t.vx.p, t.vb.p, st);
     convert<float, double>(ctx, L.ndofs, t.vx.p, z, st);
   }
+}
+
+// V-cycle on the PCG work vectors as a CUDA graph: the ~20 launches per level are captured once (on an
+// internal stream, since the legacy stream cannot be captured) and replayed on the caller's stream.
+bool same_mg(const c0ip_mg_config& a, const c0ip_mg_config& b) {
+  return a.smoother == b.smoother && a.steps == b.steps && a.omega == b.omega && a.symmetric == b.symmetric &&
+         a.cycle_dtype == b.cycle_dtype;
+}
+
+void vcycle_graph(c0ip_ctx ctx, const c0ip_mg_config& mg, const double* r, double* z, cudaStream_t st) {
+  if (!ctx->vc_exec || !same_mg(ctx->vc_key, mg)) {
+    if (ctx->vc_exec) { cudaGraphExecDestroy(ctx->vc_exec); ctx->vc_exec = nullptr; }
+    if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    CK(cudaStreamSynchronize(st));
+    const int64_t l0 = ctx->launches;
+    CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      vcycle_top(ctx, mg, r, z, ctx->cap_stream);
+    } catch (...) {
+      cudaGraph_t g;
+      cudaStreamEndCapture(ctx->cap_stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraph_t g;
+    CK(cudaStreamEndCapture(ctx->cap_stream, &g));
+    cudaError_t e = cudaGraphInstantiate(&ctx->vc_exec, g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+    ctx->vc_key = mg;
+    ctx->vc_nodes = ctx->launches - l0;
+    ctx->launches = l0;
+  }
+  CK(cudaGraphLaunch(ctx->vc_exec, st));
+  ctx->launches += ctx->vc_nodes;
 }
 
 // dots[i] = <x_i, y_i>, i < nd, read back to host (synchronises the stream)
@@ -843,7 +885,7 @@ c0ip_status c0ip_pcg(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, do
     rn = std::sqrt(dd[0]);
     if (res_history) res_history[it] = rn;
     if (rn <= rtol * r0) break;
-    vcycle_top(ctx, *mg, r, z, st);
+    vcycle_graph(ctx, *mg, r, z, st);
     dots(ctx, n, 1, r, z, nullptr, nullptr, nullptr, nullptr, dd, st);
     const double beta = dd[0] / rz;
     rz = dd[0];

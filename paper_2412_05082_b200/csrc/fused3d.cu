@@ -48,10 +48,11 @@ struct Apply3Layout {
   static constexpr int C = Tile3<K>::C, O = Tile3<K>::O;
   static constexpr int BW = (C + 3) * K + 1;      // in-plane box [(c0-2)K, (c0+C+1)K]
   static constexpr int PX = odd(BW), PO = odd(O);
-  static constexpr int XB = K * BW * PX;          // K planes of the box
+  static constexpr int XB = K * BW * PX;          // K planes of the box (double buffered)
   static constexpr int SX = K * 3 * BW * PO;      // x-stage outputs (B, L, M) of K planes
   static constexpr int PQR = K * 3 * O * O;       // in-plane results of K planes
-  static constexpr int TOTAL = XB + SX + PQR;
+  static constexpr int TOTAL = 2 * XB + SX + PQR;
+  static constexpr int MINB = (K <= 3) ? 2 : 1;   // CTAs per SM (registers / shared memory)
 };
 
 // banded row of class PP applied to a window w (w index o <-> offset o - 2K around the output node)
@@ -67,15 +68,34 @@ __device__ __forceinline__ T row_band(F coef, const T* w, int base) {
   return s;
 }
 
+// K node planes z0 .. z0+K-1 of the in-plane box into smem (cp.async, zero fill outside the domain)
+template <typename T, int K, int BW, int PX>
+__device__ __forceinline__ void load_planes_async(T* dst, const T* src, int64_t n, int64_t KN, int64_t z0,
+                                                  int64_t Y0, int64_t X0) {
+  const bool inner = (X0 >= 1 && X0 + BW - 1 <= KN - 1 && Y0 >= 1 && Y0 + BW - 1 <= KN - 1 && z0 >= 1 &&
+                      z0 + K - 1 <= KN - 1);
+  const T* base = src + ((z0 - 1) * n + (Y0 - 1)) * n + (X0 - 1);
+  for (int e = threadIdx.x; e < K * BW * BW; e += blockDim.x) {
+    const int pz = e / (BW * BW), rem = e - pz * (BW * BW), r = rem / BW, cc = rem - (rem / BW) * BW;
+    const int64_t off = ((int64_t)pz * n + r) * n + cc;
+    bool ok = inner;
+    if (!inner) {
+      const int64_t jz = z0 + pz, jy = Y0 + r, jx = X0 + cc;
+      ok = (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1 && jz >= 1 && jz <= KN - 1);
+    }
+    cp_async_elem(dst + (pz * BW + r) * PX + cc, ok ? base + off : src, ok);
+  }
+}
+
 template <typename T, int K>
-__global__ void __launch_bounds__(256, 1) apply3d_kernel(const __grid_constant__ Apply3P<T, K> P) {
+__global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(const __grid_constant__ Apply3P<T, K> P) {
   using LY = Apply3Layout<T, K>;
   constexpr int C = LY::C, O = LY::O, BW = LY::BW, PX = LY::PX, PO = LY::PO, CZ = Tile3<K>::CZ;
   constexpr int NT = 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  T* xb = sm;                     // [K][BW][PX]
-  T* sx = xb + LY::XB;            // [K][3][BW][PO]  (0: B^x, 1: L^x, 2: M^x)
+  T* const xb0 = sm;              // [2][K][BW][PX]
+  T* sx = xb0 + 2 * LY::XB;       // [K][3][BW][PO]  (0: B^x, 1: L^x, 2: M^x)
   T* pqr = sx + LY::SX;           // [K][3][O][O]    (0: P, 1: Q, 2: R)
   const int64_t N = P.N, n = P.n, KN = K * N;
   const int ntx = int((N + C - 1) / C);
@@ -92,18 +112,18 @@ __global__ void __launch_bounds__(256, 1) apply3d_kernel(const __grid_constant__
   int round = 0;
   const int nsteps = int(std::min<int64_t>(CZ, N - cz0)) + 4;
 
+  // prefetch pipeline: the K planes of step s + 1 load while step s computes
+  load_planes_async<T, K, BW, PX>(xb0, P.x, n, KN, (cz0 - 3) * K + 1, (cy0 - 2) * K, (cx0 - 2) * K);
+  cp_async_commit();
   for (int s = 0; s < nsteps; ++s) {
-    // node planes of this step: zp = (cz0 - 3 + s) K + 1 + pz, pz < K
-    const int64_t z0 = (cz0 - 3 + s) * K + 1;
-    for (int e = tid; e < K * BW * BW; e += NT) {
-      const int pz = e / (BW * BW), rem = e - pz * (BW * BW), r = rem / BW, cc = rem - (rem / BW) * BW;
-      const int64_t jz = z0 + pz, jy = (cy0 - 2) * K + r, jx = (cx0 - 2) * K + cc;
-      T v = 0;
-      if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1 && jz >= 1 && jz <= KN - 1)
-        v = P.x[((jz - 1) * n + (jy - 1)) * n + (jx - 1)];
-      xb[(pz * BW + r) * PX + cc] = v;
-    }
+    // node planes of this step: (cz0 - 3 + s) K + 1 + pz, pz < K
+    if (s + 1 < nsteps)
+      load_planes_async<T, K, BW, PX>(xb0 + ((s + 1) & 1) * LY::XB, P.x, n, KN, (cz0 - 2 + s) * K + 1,
+                                      (cy0 - 2) * K, (cx0 - 2) * K);
+    cp_async_commit();
+    cp_async_wait1();
     __syncthreads();
+    const T* xb = xb0 + (s & 1) * LY::XB;
 
     // x-stage: unit = (plane, box row, cell) -> B^ L^ M^ along x for the K nodes of the cell
 #pragma unroll 1

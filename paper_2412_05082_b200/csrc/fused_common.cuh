@@ -58,8 +58,8 @@ struct Tile {
 
 template <typename T, int K>
 struct Blk {
-  // register blocking factor (lines per thread sharing one coefficient load)
-  static constexpr int RB = (sizeof(T) == 8) ? (K <= 5 ? 2 : 1) : 2;
+  // maximum register-blocking factor (lines per thread sharing one coefficient load)
+  static constexpr int RB = (sizeof(T) == 8) ? (K <= 3 ? 3 : (K <= 5 ? 2 : 1)) : (K <= 5 ? 3 : 2);
 };
 
 __host__ __device__ constexpr int odd(int v) { return v | 1; }

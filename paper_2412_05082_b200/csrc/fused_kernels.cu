@@ -34,6 +34,17 @@
 
 namespace c0ip {
 
+// register-blocking factor of a stage with `lines` lines per unit column and `mult` unit columns:
+// minimise rounds(rb) * rb over 256 threads (the per-thread work of a stage), prefer larger rb on ties
+__host__ __device__ constexpr int pick_rb(int lines, int mult, int maxrb) {
+  int best = 1, bestc = 1 << 30;
+  for (int rb = 1; rb <= maxrb; ++rb) {
+    const int cost = cdiv(cdiv(lines, rb) * mult, 256) * rb;
+    if (cost <= bestc) { bestc = cost; best = rb; }
+  }
+  return best;
+}
+
 // ----------------------------------------------------------------------------- apply2d
 template <typename T, int K>
 struct ApplyLayout {
@@ -43,14 +54,15 @@ struct ApplyLayout {
   static constexpr int XB = BW * PX, BB = O * PO;  // box, b tile
   static constexpr int STAGE = BW * PO;            // one of the three x-stage outputs
   static constexpr int TOTAL = 2 * (XB + BB) + 3 * STAGE;
-  static constexpr int GX = cdiv(BW, RB);          // row groups of the x-stage
-  static constexpr int GY = cdiv(O, RB);           // column groups of the y-stage
+  static constexpr int RBX = pick_rb(BW, C, RB), RBY = pick_rb(O, C, RB);
+  static constexpr int GX = cdiv(BW, RBX);         // row groups of the x-stage
+  static constexpr int GY = cdiv(O, RBY);          // column groups of the y-stage
 };
 
 template <typename T, int K>
 __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__ ApplyP<T, K> P) {
   using LY = ApplyLayout<T, K>;
-  constexpr int C = LY::C, O = LY::O, BW = LY::BW, PX = LY::PX, PO = LY::PO, RB = LY::RB;
+  constexpr int C = LY::C, O = LY::O, BW = LY::BW, PX = LY::PX, PO = LY::PO;
   constexpr int GX = LY::GX, GY = LY::GY;
   constexpr int NT = 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -89,6 +101,7 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
     // a thread holds rows g, g + GX, ... (RB rows) of one cell and reuses every coefficient RB times.
 #pragma unroll 1
     for (int it = 0; it < cdiv(GX * C, NT); ++it, ++round) {
+      constexpr int RB = LY::RBX;
       const int u = it * NT + tid;
       if (u >= GX * C) continue;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
@@ -138,6 +151,7 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
     // groups; three passes (one window at a time) accumulate K outputs for RB columns.
 #pragma unroll 1
     for (int it = 0; it < cdiv(GY * C, NT); ++it, ++round) {
+      constexpr int RB = LY::RBY;
       const int u = it * NT + tid;
       if (u >= GY * C) continue;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
@@ -289,9 +303,12 @@ struct FdmLayout {
   static constexpr int Z1 = RN * PE;               // Z1 [RN][E]; later Z3 [O][E]
   static constexpr int Z2 = (C + 1) * NP * PE;     // Z2 [vy][iy][E]; later out staging [O][PS]
   static constexpr int TOTAL = 2 * (RB_ + XT) + Z1 + Z2 + NP * NP;
-  static constexpr int GR = cdiv(RN, RB);          // FX row groups
-  static constexpr int GE = cdiv(E, RB);           // FYg / FYs column groups
-  static constexpr int GO = cdiv(O, RB);           // FS row groups
+  static constexpr int RB_FX = pick_rb(RN, C + 1, RB), RB_G = pick_rb(E, C + 1, RB);
+  static constexpr int RB_S = pick_rb(E, C, RB), RB_O = pick_rb(O, C, RB);
+  static constexpr int GR = cdiv(RN, RB_FX);       // FX row groups
+  static constexpr int GEG = cdiv(E, RB_G);        // FYg column groups
+  static constexpr int GES = cdiv(E, RB_S);        // FYs column groups
+  static constexpr int GO = cdiv(O, RB_O);         // FS row groups
 };
 
 // x += omega h^2 sum_v R_v^T A~_v^{-1} R_v r on the tile (gather form, see file header):
@@ -302,8 +319,8 @@ struct FdmLayout {
 template <typename T, int K>
 __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ FdmP<T, K> P) {
   using LY = FdmLayout<T, K>;
-  constexpr int C = LY::C, O = LY::O, NP = LY::NP, RN = LY::RN, E = LY::E, RB = LY::RB;
-  constexpr int PR = LY::PR, PE = LY::PE, PS = LY::PS, GR = LY::GR, GE = LY::GE, GO = LY::GO;
+  constexpr int C = LY::C, O = LY::O, NP = LY::NP, RN = LY::RN, E = LY::E;
+  constexpr int PR = LY::PR, PE = LY::PE, PS = LY::PS, GR = LY::GR, GO = LY::GO;
   constexpr int NT = 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
@@ -347,6 +364,7 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
     // FX: lanes <-> row groups, one patch vx per unit (uniform variant)
 #pragma unroll 1
     for (int it = 0; it < cdiv(GR * (C + 1), NT); ++it, ++round) {
+      constexpr int RB = LY::RB_FX;
       const int u = it * NT + tid;
       if (u >= GR * (C + 1)) continue;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
@@ -380,7 +398,8 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 
     // FYg: lanes <-> column groups, one patch row vy per unit
 #pragma unroll 1
-    for (int it = 0; it < cdiv(GE * (C + 1), NT); ++it, ++round) {
+    for (int it = 0; it < cdiv(LY::GEG * (C + 1), NT); ++it, ++round) {
+      constexpr int RB = LY::RB_G, GE = LY::GEG;
       const int u = it * NT + tid;
       if (u >= GE * (C + 1)) continue;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
@@ -432,7 +451,8 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 
     // FYs: lanes <-> column groups, one cell row cy per unit: rows cyK .. cyK+K-1
 #pragma unroll 1
-    for (int it = 0; it < cdiv(GE * C, NT); ++it, ++round) {
+    for (int it = 0; it < cdiv(LY::GES * C, NT); ++it, ++round) {
+      constexpr int RB = LY::RB_S, GE = LY::GES;
       const int u = it * NT + tid;
       if (u >= GE * C) continue;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
@@ -461,6 +481,7 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
     // FS: lanes <-> row groups, one cell column cx per unit
 #pragma unroll 1
     for (int it = 0; it < cdiv(GO * C, NT); ++it, ++round) {
+      constexpr int RB = LY::RB_O;
       const int u = it * NT + tid;
       if (u >= GO * C) continue;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
