@@ -128,9 +128,9 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
     // x-stage: unit = (plane, box row, cell) -> B^ L^ M^ along x for the K nodes of the cell
 #pragma unroll 1
     for (int it = 0; it < cdiv(K * BW * C, NT); ++it, ++round) {
+      const Coef2<T, K>& c = coef_at(P.c, (s + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= K * BW * C) continue;
-      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int r = u % BW, rest = u / BW, ci = rest % C, pz = rest / C;
       const int64_t cx = cx0 + ci;
       if (cx >= N) continue;
@@ -164,9 +164,9 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
     // y-stage: unit = (plane, owned column, cell row) -> P, Q, R for the K nodes of the cell row
 #pragma unroll 1
     for (int it = 0; it < cdiv(K * O * C, NT); ++it, ++round) {
+      const Coef2<T, K>& c = coef_at(P.c, (s + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= K * O * C) continue;
-      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int col = u % O, rest = u / O, ci = rest % C, pz = rest / C;
       const int64_t cy = cy0 + ci;
       if (cy >= N) continue;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
     if (s >= 4 && zown) {
       const int64_t jx = cx0 * K + ox, jy = cy0 * K + oy;
       if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1) {
-        const Coef2<T, K>& c = coef_at(P.c, (round++) * P.zero);
+        const Coef2<T, K>& c = coef_at(P.c, (s + 1000) * P.zero);
         const bool inner = (cz >= 2 && cz <= N - 2);
 #pragma unroll
         for (int p = 0; p < K; ++p) {
@@ -311,51 +311,52 @@ __global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_consta
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* buf0 = reinterpret_cast<T*>(smem_raw);
   T* buf1 = buf0 + PB * NL;
+  __shared__ int64_t gbase[PB];       // global index of the patch's first DoF (or -1)
+  __shared__ int8_t pvar[PB][3];      // axis variants
   const int64_t N = P.N, n = P.n;
-  const int64_t first = (int64_t)blockIdx.x * PB;
   const int tid = threadIdx.x;
   int round = 0;
-  auto vert = [&](int p, int64_t* v) -> bool {
-    const int64_t q = first + p;
-    if (q >= P.count) return false;
-    const int64_t pid = P.list ? P.list[q] : q;
-    v[0] = 1 + pid % (N - 1);
-    v[1] = 1 + (pid / (N - 1)) % (N - 1);
-    v[2] = 1 + pid / ((N - 1) * (N - 1));
-    return true;
-  };
+  if (tid < PB) {
+    const int64_t q = (int64_t)blockIdx.x * PB + tid;
+    if (q < P.count) {
+      const int pid = P.list ? P.list[q] : (int)q;
+      const int Nm1 = (int)(N - 1);
+      const int vx = 1 + pid % Nm1, vy = 1 + (pid / Nm1) % Nm1, vz = 1 + pid / (Nm1 * Nm1);
+      gbase[tid] = (((int64_t)(vz - 1) * K) * n + (int64_t)(vy - 1) * K) * n + (int64_t)(vx - 1) * K;
+      pvar[tid][0] = (int8_t)variant_of(vx, N);
+      pvar[tid][1] = (int8_t)variant_of(vy, N);
+      pvar[tid][2] = (int8_t)variant_of(vz, N);
+    } else {
+      gbase[tid] = -1;
+    }
+  }
+  __syncthreads();
   // gather R_v r
   for (int e = tid; e < PB * NL; e += NT) {
     const int p = e / NL, l = e - p * NL;
-    int64_t v[3];
-    T val = 0;
-    if (vert(p, v)) {
-      const int lx = l % NP, ly = (l / NP) % NP, lz = l / (NP * NP);
-      val = P.r[(((v[2] - 1) * K + lz) * n + (v[1] - 1) * K + ly) * n + (v[0] - 1) * K + lx];
-    }
-    buf0[e] = val;
+    const int lx = l % NP, ly = (l / NP) % NP, lz = l / (NP * NP);
+    const int64_t g0 = gbase[p];
+    buf0[e] = g0 >= 0 ? P.r[g0 + ((int64_t)lz * n + ly) * n + lx] : T(0);
   }
   __syncthreads();
   T* in = buf0;
   T* out = buf1;
-  // S^T along x, y, z; divide; S along z, y, x  (lines: one per thread, units = (patch, line))
+  // S^T along x, y, z; divide; S along z, y, x  (one thread per patch line; units = (patch, line))
 #pragma unroll
   for (int stage = 0; stage < 6; ++stage) {
     const int ax = stage < 3 ? stage : 5 - stage;
 #pragma unroll 1
     for (int it = 0; it < cdiv(PB * NP * NP, NT); ++it, ++round) {
+      const Coef2<T, K>& c = coef_at(P.c, (stage + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= PB * NP * NP) continue;
-      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int p = u / (NP * NP), li = u - p * (NP * NP);
-      int64_t v[3];
-      if (!vert(p, v)) continue;
-      const int var = variant_of(v[ax], N);
-      // line start: the two other local coordinates from li
+      if (gbase[p] < 0) continue;
+      const int var = pvar[p][ax];
       int base;
-      if (ax == 0) base = li * NP;                                   // (ly, lz) = li
-      else if (ax == 1) base = (li / NP) * NP * NP + (li % NP);      // (lx, lz)
-      else base = li;                                                // (lx, ly)
+      if (ax == 0) base = li * NP;                                   // line (ly, lz)
+      else if (ax == 1) base = (li / NP) * NP * NP + (li % NP);      // line (lx, lz)
+      else base = li;                                                // line (lx, ly)
       T* o = out + p * NL + base;
       const T* ii = in + p * NL + base;
       if (ax == 0) { if (stage < 3) contract3<T, K, 0, true>(c, var, ii, o); else contract3<T, K, 0, false>(c, var, ii, o); }
@@ -367,11 +368,9 @@ __global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_consta
     if (stage == 2) {
       for (int e = tid; e < PB * NL; e += NT) {
         const int p = e / NL, l = e - p * NL;
-        int64_t v[3];
-        if (!vert(p, v)) continue;
+        if (gbase[p] < 0) continue;
         const int lx = l % NP, ly = (l / NP) % NP, lz = l / (NP * NP);
-        in[e] /= (P.c.lam[variant_of(v[0], N)][lx] + P.c.lam[variant_of(v[1], N)][ly] +
-                  P.c.lam[variant_of(v[2], N)][lz]);
+        in[e] /= (P.c.lam[pvar[p][0]][lx] + P.c.lam[pvar[p][1]][ly] + P.c.lam[pvar[p][2]][lz]);
       }
       __syncthreads();
     }
@@ -379,10 +378,10 @@ __global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_consta
   // scatter: x += omega h u  (disjoint patches within one launch: plain read-modify-write)
   for (int e = tid; e < PB * NL; e += NT) {
     const int p = e / NL, l = e - p * NL;
-    int64_t v[3];
-    if (!vert(p, v)) continue;
+    const int64_t g0 = gbase[p];
+    if (g0 < 0) continue;
     const int lx = l % NP, ly = (l / NP) % NP, lz = l / (NP * NP);
-    const int64_t g = (((v[2] - 1) * K + lz) * n + (v[1] - 1) * K + ly) * n + (v[0] - 1) * K + lx;
+    const int64_t g = g0 + ((int64_t)lz * n + ly) * n + lx;
     P.x[g] = fma(P.factor, in[e], P.x[g]);
   }
 }

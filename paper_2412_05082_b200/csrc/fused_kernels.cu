@@ -97,17 +97,20 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
     const T* bt = bbuf0 + buf * LY::BB;
     const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(ty0 + t / ntx) * C;
 
+    const bool tin = (cx0 >= 2 && cx0 + C - 1 <= N - 2 && cy0 >= 2 && cy0 + C - 1 <= N - 2);
+    auto tile_body = [&](auto INC) {
+      constexpr bool IN = decltype(INC)::value;
     // x-stage: B^_x x, L^_x x, M^_x x on all box rows, owned columns.  lanes <-> row groups;
     // a thread holds rows g, g + GX, ... (RB rows) of one cell and reuses every coefficient RB times.
 #pragma unroll 1
     for (int it = 0; it < cdiv(GX * C, NT); ++it, ++round) {
       constexpr int RB = LY::RBX;
+      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GX * C) continue;
-      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GX, ci = u / GX;
       const int64_t cx = cx0 + ci;
-      if (cx >= N) continue;
+      if (!IN && cx >= N) continue;
       T w[RB][4 * K + 1];
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
 #pragma unroll
         for (int q = 0; q <= 4 * K; ++q) w[r][q] = xb[row * PX + ci * K + q];
       }
-      const bool inner = (cx >= 2 && cx <= N - 2);
+      const bool inner = IN || (cx >= 2 && cx <= N - 2);
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         T ob[RB], ol[RB], om[RB];
@@ -152,13 +155,13 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
 #pragma unroll 1
     for (int it = 0; it < cdiv(GY * C, NT); ++it, ++round) {
       constexpr int RB = LY::RBY;
+      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GY * C) continue;
-      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GY, ci = u / GY;
       const int64_t cy = cy0 + ci;
-      if (cy >= N) continue;
-      const bool inner = (cy >= 2 && cy <= N - 2);
+      if (!IN && cy >= N) continue;
+      const bool inner = IN || (cy >= 2 && cy <= N - 2);
       T acc[K][RB];
 #pragma unroll
       for (int p = 0; p < K; ++p)
@@ -215,16 +218,19 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
       for (int r = 0; r < RB; ++r) {
         const int cc = g + r * GY;
         const int64_t jx = cx0 * K + cc;
-        if (cc >= O || jx < 1 || jx > KN - 1) continue;
+        if (cc >= O || (!IN && (jx < 1 || jx > KN - 1))) continue;
 #pragma unroll
         for (int p = 0; p < K; ++p) {
           const int64_t j = cy * K + p;
-          if (j < P.out_lo || j >= P.out_hi) continue;
+          if (j < P.out_lo || j >= P.out_hi) continue;   // (slab window; always true for the full domain)
           const T v = P.scale * acc[p][r];
           P.y[(j - 1 - P.row0) * n + (jx - 1)] = P.b ? bt[(ci * K + p) * PO + cc] - v : v;
         }
       }
     }
+    };
+    if (tin) tile_body(std::true_type{});
+    else tile_body(std::false_type{});
     __syncthreads();
     buf ^= 1;
   }
@@ -361,17 +367,22 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
     const T* xt = xbuf0 + buf * LY::XT;
     const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(ty0 + t / ntx) * C;
 
+    // interior tiles (every patch of the tile has the interior variant on both axes) take a
+    // specialised path without variant / range checks
+    const bool tin = (cx0 >= 2 && cx0 + C <= N - 2 && cy0 >= 2 && cy0 + C <= N - 2);
+    auto tile_body = [&](auto INC) {
+      constexpr bool IN = decltype(INC)::value;
     // FX: lanes <-> row groups, one patch vx per unit (uniform variant)
 #pragma unroll 1
     for (int it = 0; it < cdiv(GR * (C + 1), NT); ++it, ++round) {
       constexpr int RB = LY::RB_FX;
+      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GR * (C + 1)) continue;
-      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GR, pi = u / GR;
       const int64_t vx = cx0 + pi;
       T z[RB][NP];
-      if (vx >= 1 && vx <= N - 1) {
+      if (IN || (vx >= 1 && vx <= N - 1)) {
         T w[RB][NP];
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
@@ -379,7 +390,8 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 #pragma unroll
           for (int l = 0; l < NP; ++l) w[r][l] = rb[row * PR + pi * K + l];
         }
-        s_t_var<T, K, 1, RB>(variant_of(vx, N), c, w, z);
+        if constexpr (IN) s_t<T, K, 1, RB>(c, w, z);
+        else s_t_var<T, K, 1, RB>(variant_of(vx, N), c, w, z);
       } else {
 #pragma unroll
         for (int r = 0; r < RB; ++r)
@@ -400,25 +412,32 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 #pragma unroll 1
     for (int it = 0; it < cdiv(LY::GEG * (C + 1), NT); ++it, ++round) {
       constexpr int RB = LY::RB_G, GE = LY::GEG;
+      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GE * (C + 1)) continue;
-      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GE, qi = u / GE;
       const int64_t vy = cy0 + qi;
       int col[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) col[r] = min(g + r * GE, E - 1);
       T z[RB][NP];
-      if (vy >= 1 && vy <= N - 1) {
+      if (IN || (vy >= 1 && vy <= N - 1)) {
         T w[RB][NP];
 #pragma unroll
         for (int r = 0; r < RB; ++r)
 #pragma unroll
           for (int l = 0; l < NP; ++l) w[r][l] = z1[(qi * K + l) * PE + col[r]];
-        const int vary = variant_of(vy, N);
-        s_t_var<T, K, 1, RB>(vary, c, w, z);
+        const int vary = IN ? 1 : variant_of(vy, N);
+        if constexpr (IN) s_t<T, K, 1, RB>(c, w, z);
+        else s_t_var<T, K, 1, RB>(vary, c, w, z);
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
+          if constexpr (IN) {
+            const int ix = col[r] - (col[r] / NP) * NP;
+#pragma unroll
+            for (int i = 0; i < NP; ++i) z[r][i] *= invd[i * NP + ix];
+            continue;
+          }
           const int pi = col[r] / NP, ix = col[r] - (col[r] / NP) * NP;
           const int64_t vx = cx0 + pi;
           if (vx < 1 || vx > N - 1) {
@@ -453,9 +472,9 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 #pragma unroll 1
     for (int it = 0; it < cdiv(LY::GES * C, NT); ++it, ++round) {
       constexpr int RB = LY::RB_S, GE = LY::GES;
+      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GE * C) continue;
-      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GE, ci = u / GE;
       T a0[RB][NP], a1[RB][NP], out[RB][K];
 #pragma unroll
@@ -467,7 +486,16 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
           a1[r][i] = z2[((ci + 1) * NP + i) * PE + cc];
         }
       }
-      cell_from_patches<T, K, RB>(c, cy0 + ci, N, a0, a1, out);
+      if constexpr (IN) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int p = 0; p < K; ++p) out[r][p] = 0;
+        s_rows<T, K, 1, K - 1, 0, RB>(c, a0, out);
+        s_rows<T, K, 1, -1, 1, RB>(c, a1, out);
+      } else {
+        cell_from_patches<T, K, RB>(c, cy0 + ci, N, a0, a1, out);
+      }
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
         const int cc = g + r * GE;
@@ -482,9 +510,9 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 #pragma unroll 1
     for (int it = 0; it < cdiv(GO * C, NT); ++it, ++round) {
       constexpr int RB = LY::RB_O;
+      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GO * C) continue;
-      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GO, ci = u / GO;
       T a0[RB][NP], a1[RB][NP], out[RB][K];
 #pragma unroll
@@ -496,7 +524,16 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
           a1[r][i] = z3[oy * PE + (ci + 1) * NP + i];
         }
       }
-      cell_from_patches<T, K, RB>(c, cx0 + ci, N, a0, a1, out);
+      if constexpr (IN) {
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+#pragma unroll
+          for (int p = 0; p < K; ++p) out[r][p] = 0;
+        s_rows<T, K, 1, K - 1, 0, RB>(c, a0, out);
+        s_rows<T, K, 1, -1, 1, RB>(c, a1, out);
+      } else {
+        cell_from_patches<T, K, RB>(c, cx0 + ci, N, a0, a1, out);
+      }
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
         const int oy = g + r * GO;
@@ -506,6 +543,10 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
       }
     }
     __syncthreads();
+
+    };
+    if (tin) tile_body(std::true_type{});
+    else tile_body(std::false_type{});
 
     for (int e = tid; e < O * O; e += NT) {
       const int oy = e / O, ox = e - (e / O) * O;
@@ -563,13 +604,22 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   auto sX = [&](int p, int which) { return sm + p * PER + BX * BX + which * BX * NP; };
   auto rr = [&](int p) { return sm + p * PER + BX * BX + 3 * BX * NP; };
   auto zz = [&](int p) { return rr(p) + NP * NP; };
+  __shared__ int pv[PB][2];            // patch vertices (0 = no patch)
+  if (tid < PB) {
+    const int64_t q = first + tid;
+    if (q < P.count) {
+      const int pid = P.list[q], Nm1 = (int)(N - 1);
+      pv[tid][0] = 1 + pid % Nm1;
+      pv[tid][1] = 1 + pid / Nm1;
+    } else {
+      pv[tid][0] = pv[tid][1] = 0;
+    }
+  }
+  __syncthreads();
   auto vert = [&](int p, int64_t& vx, int64_t& vy) -> bool {
-    const int64_t q = first + p;
-    if (q >= P.count) return false;
-    const int64_t pid = P.list[q];
-    vx = 1 + pid % (N - 1);
-    vy = 1 + pid / (N - 1);
-    return true;
+    vx = pv[p][0];
+    vy = pv[p][1];
+    return vx != 0;
   };
 
   // 0. x boxes [(v-2)K, (v+2)K]^2 and b on the patch nodes
@@ -595,9 +645,9 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   // 1. x-stage on every box row, patch columns only: B^_x, L^_x, M^_x.  unit = (patch, box row).
 #pragma unroll 1
   for (int it = 0; it < cdiv(PB * BX, NT); ++it, ++round) {
+    const Coef2<T, K>& c = coef_at(P.c, it * P.zero);
     const int u = it * NT + tid;
     if (u >= PB * BX) continue;
-    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     const int p = u / BX, r = u - (u / BX) * BX;
     int64_t vx, vy;
     if (!vert(p, vx, vy)) continue;
@@ -644,9 +694,9 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   // 2. y-stage: r = b - h^-2 (B^_y(M^x) + M^_y(B^x) + 2 L^_y(L^x)) on the patch rows.  unit = (patch, col).
 #pragma unroll 1
   for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
+    const Coef2<T, K>& c = coef_at(P.c, it * P.zero);
     const int u = it * NT + tid;
     if (u >= PB * NP) continue;
-    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     const int p = u / NP, l = u - (u / NP) * NP;
     int64_t vx, vy;
     if (!vert(p, vx, vy)) continue;
@@ -694,9 +744,9 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   // 3. FDM: FX rows (S_vx^T), FY columns (S_vy^T, divide, S_vy), FS rows (S_vx) + update.
 #pragma unroll 1
   for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
+    const Coef2<T, K>& c = coef_at(P.c, it * P.zero);
     const int u = it * NT + tid;
     if (u >= PB * NP) continue;
-    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     const int p = u / NP, i = u - (u / NP) * NP;
     int64_t vx, vy;
     if (!vert(p, vx, vy)) continue;
@@ -710,9 +760,9 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   __syncthreads();
 #pragma unroll 1
   for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
+    const Coef2<T, K>& c = coef_at(P.c, it * P.zero);
     const int u = it * NT + tid;
     if (u >= PB * NP) continue;
-    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     const int p = u / NP, j = u - (u / NP) * NP;
     int64_t vx, vy;
     if (!vert(p, vx, vy)) continue;
@@ -744,9 +794,9 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   __syncthreads();
 #pragma unroll 1
   for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
+    const Coef2<T, K>& c = coef_at(P.c, it * P.zero);
     const int u = it * NT + tid;
     if (u >= PB * NP) continue;
-    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     const int p = u / NP, i = u - (u / NP) * NP;
     int64_t vx, vy;
     if (!vert(p, vx, vy)) continue;
