@@ -338,7 +338,9 @@ void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, b
       continue;
     apply_op<T>(ctx, L, x, b, t.sres.p, st);                     // one residual per AVS step
     if (sm == C0IP_AVS_ATOMIC) {
-      patch_solve<T>(ctx, L, t.sres.p, x, omega, nullptr, L.npatch, 1, st);
+      if (!(ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
+            c0ip::fused3_patch_fdm<T>(*L.fused, omega, t.sres.p, x, nullptr, L.npatch, st, &ctx->launches, 1)))
+        patch_solve<T>(ctx, L, t.sres.p, x, omega, nullptr, L.npatch, 1, st);
     } else {   // coloured / deterministic generic: serialise writes over the 2^d parity classes
       for (int c = 0; c < (1 << d); ++c) {
         int64_t cnt = L.parity_off[c + 1] - L.parity_off[c];

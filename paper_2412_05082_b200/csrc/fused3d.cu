@@ -128,9 +128,9 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
     // x-stage: unit = (plane, box row, cell) -> B^ L^ M^ along x for the K nodes of the cell
 #pragma unroll 1
     for (int it = 0; it < cdiv(K * BW * C, NT); ++it, ++round) {
-      const Coef2<T, K>& c = coef_at(P.c, (s + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= K * BW * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int r = u % BW, rest = u / BW, ci = rest % C, pz = rest / C;
       const int64_t cx = cx0 + ci;
       if (cx >= N) continue;
@@ -164,9 +164,9 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
     // y-stage: unit = (plane, owned column, cell row) -> P, Q, R for the K nodes of the cell row
 #pragma unroll 1
     for (int it = 0; it < cdiv(K * O * C, NT); ++it, ++round) {
-      const Coef2<T, K>& c = coef_at(P.c, (s + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= K * O * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int col = u % O, rest = u / O, ci = rest % C, pz = rest / C;
       const int64_t cy = cy0 + ci;
       if (cy >= N) continue;
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
     if (s >= 4 && zown) {
       const int64_t jx = cx0 * K + ox, jy = cy0 * K + oy;
       if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1) {
-        const Coef2<T, K>& c = coef_at(P.c, (s + 1000) * P.zero);
+        const Coef2<T, K>& c = coef_at(P.c, (round++) * P.zero);
         const bool inner = (cz >= 2 && cz <= N - 2);
 #pragma unroll
         for (int p = 0; p < K; ++p) {
@@ -271,6 +271,7 @@ struct Fdm3P {
   int64_t N, n;
   T factor;                 // omega h (A~^-1 = h A^~^-1 in 3D)
   int zero;
+  int atomic;               // 1: overlapping patches (atomic AVS, red.global.add), 0: disjoint list
 };
 
 template <typename T, int K>
@@ -347,9 +348,9 @@ __global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_consta
     const int ax = stage < 3 ? stage : 5 - stage;
 #pragma unroll 1
     for (int it = 0; it < cdiv(PB * NP * NP, NT); ++it, ++round) {
-      const Coef2<T, K>& c = coef_at(P.c, (stage + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= PB * NP * NP) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int p = u / (NP * NP), li = u - p * (NP * NP);
       if (gbase[p] < 0) continue;
       const int var = pvar[p][ax];
@@ -382,7 +383,8 @@ __global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_consta
     if (g0 < 0) continue;
     const int lx = l % NP, ly = (l / NP) % NP, lz = l / (NP * NP);
     const int64_t g = g0 + ((int64_t)lz * n + ly) * n + lx;
-    P.x[g] = fma(P.factor, in[e], P.x[g]);
+    if (P.atomic) atomicAdd(P.x + g, P.factor * in[e]);
+    else P.x[g] = fma(P.factor, in[e], P.x[g]);
   }
 }
 
@@ -408,7 +410,7 @@ static void launch_apply3(const FusedLevel& F, const T* x, const T* b, T* y, cud
 
 template <typename T, int K>
 static void launch_fdm3(const FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
-                        cudaStream_t st) {
+                        int atomic, cudaStream_t st) {
   using LY = Fdm3Layout<T, K>;
   const size_t smem = sizeof(T) * size_t(LY::TOTAL);
   static bool attr = false;
@@ -422,6 +424,7 @@ static void launch_fdm3(const FusedLevel& F, T omega, const T* r, T* x, const in
   p.r = r; p.x = x; p.list = list; p.count = count; p.N = F.N; p.n = F.n;
   p.factor = T(double(omega) * F.h);
   p.zero = 0;
+  p.atomic = atomic;
   const int64_t grid = (count + LY::PB - 1) / LY::PB;
   patch_fdm3d_kernel<T, K><<<(unsigned)grid, 256, smem, st>>>(p);
 }
@@ -448,14 +451,14 @@ bool fused3_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, 
 
 template <typename T>
 bool fused3_patch_fdm(FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
-                      cudaStream_t st, int64_t* launches) {
+                      cudaStream_t st, int64_t* launches, int atomic) {
   if (F.d != 3) return false;
   if (count == 0) return true;
   switch (F.k) {
-    case 2: launch_fdm3<T, 2>(F, omega, r, x, list, count, st); break;
-    case 3: launch_fdm3<T, 3>(F, omega, r, x, list, count, st); break;
-    case 4: launch_fdm3<T, 4>(F, omega, r, x, list, count, st); break;
-    case 5: launch_fdm3<T, 5>(F, omega, r, x, list, count, st); break;
+    case 2: launch_fdm3<T, 2>(F, omega, r, x, list, count, atomic, st); break;
+    case 3: launch_fdm3<T, 3>(F, omega, r, x, list, count, atomic, st); break;
+    case 4: launch_fdm3<T, 4>(F, omega, r, x, list, count, atomic, st); break;
+    case 5: launch_fdm3<T, 5>(F, omega, r, x, list, count, atomic, st); break;
     default: return false;
   }
   (*launches)++;
@@ -466,8 +469,8 @@ bool fused3_patch_fdm(FusedLevel& F, T omega, const T* r, T* x, const int32_t* l
 template bool fused3_apply<double>(FusedLevel&, const double*, const double*, double*, cudaStream_t, int64_t*);
 template bool fused3_apply<float>(FusedLevel&, const float*, const float*, float*, cudaStream_t, int64_t*);
 template bool fused3_patch_fdm<double>(FusedLevel&, double, const double*, double*, const int32_t*, int64_t,
-                                       cudaStream_t, int64_t*);
+                                       cudaStream_t, int64_t*, int);
 template bool fused3_patch_fdm<float>(FusedLevel&, float, const float*, float*, const int32_t*, int64_t,
-                                      cudaStream_t, int64_t*);
+                                      cudaStream_t, int64_t*, int);
 
 }  // namespace c0ip

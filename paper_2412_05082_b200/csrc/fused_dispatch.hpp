@@ -48,7 +48,7 @@ template <typename T>
 bool fused3_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches);
 template <typename T>
 bool fused3_patch_fdm(FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
-                      cudaStream_t st, int64_t* launches);
+                      cudaStream_t st, int64_t* launches, int atomic = 0);
 int fused_dim(const FusedLevel& F);
 
 }  // namespace c0ip

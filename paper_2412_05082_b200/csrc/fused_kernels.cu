@@ -105,9 +105,9 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
 #pragma unroll 1
     for (int it = 0; it < cdiv(GX * C, NT); ++it, ++round) {
       constexpr int RB = LY::RBX;
-      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GX * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GX, ci = u / GX;
       const int64_t cx = cx0 + ci;
       if (!IN && cx >= N) continue;
@@ -155,9 +155,9 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
 #pragma unroll 1
     for (int it = 0; it < cdiv(GY * C, NT); ++it, ++round) {
       constexpr int RB = LY::RBY;
-      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GY * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GY, ci = u / GY;
       const int64_t cy = cy0 + ci;
       if (!IN && cy >= N) continue;
@@ -376,9 +376,9 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 #pragma unroll 1
     for (int it = 0; it < cdiv(GR * (C + 1), NT); ++it, ++round) {
       constexpr int RB = LY::RB_FX;
-      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GR * (C + 1)) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GR, pi = u / GR;
       const int64_t vx = cx0 + pi;
       T z[RB][NP];
@@ -412,9 +412,9 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 #pragma unroll 1
     for (int it = 0; it < cdiv(LY::GEG * (C + 1), NT); ++it, ++round) {
       constexpr int RB = LY::RB_G, GE = LY::GEG;
-      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GE * (C + 1)) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GE, qi = u / GE;
       const int64_t vy = cy0 + qi;
       int col[RB];
@@ -472,9 +472,9 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 #pragma unroll 1
     for (int it = 0; it < cdiv(LY::GES * C, NT); ++it, ++round) {
       constexpr int RB = LY::RB_S, GE = LY::GES;
-      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GE * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GE, ci = u / GE;
       T a0[RB][NP], a1[RB][NP], out[RB][K];
 #pragma unroll
@@ -510,9 +510,9 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 #pragma unroll 1
     for (int it = 0; it < cdiv(GO * C, NT); ++it, ++round) {
       constexpr int RB = LY::RB_O;
-      const Coef2<T, K>& c = coef_at(P.c, (t + it) * P.zero);
       const int u = it * NT + tid;
       if (u >= GO * C) continue;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
       const int g = u % GO, ci = u / GO;
       T a0[RB][NP], a1[RB][NP], out[RB][K];
 #pragma unroll
@@ -645,9 +645,9 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   // 1. x-stage on every box row, patch columns only: B^_x, L^_x, M^_x.  unit = (patch, box row).
 #pragma unroll 1
   for (int it = 0; it < cdiv(PB * BX, NT); ++it, ++round) {
-    const Coef2<T, K>& c = coef_at(P.c, it * P.zero);
     const int u = it * NT + tid;
     if (u >= PB * BX) continue;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     const int p = u / BX, r = u - (u / BX) * BX;
     int64_t vx, vy;
     if (!vert(p, vx, vy)) continue;
@@ -694,9 +694,9 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   // 2. y-stage: r = b - h^-2 (B^_y(M^x) + M^_y(B^x) + 2 L^_y(L^x)) on the patch rows.  unit = (patch, col).
 #pragma unroll 1
   for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
-    const Coef2<T, K>& c = coef_at(P.c, it * P.zero);
     const int u = it * NT + tid;
     if (u >= PB * NP) continue;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     const int p = u / NP, l = u - (u / NP) * NP;
     int64_t vx, vy;
     if (!vert(p, vx, vy)) continue;
@@ -744,9 +744,9 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   // 3. FDM: FX rows (S_vx^T), FY columns (S_vy^T, divide, S_vy), FS rows (S_vx) + update.
 #pragma unroll 1
   for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
-    const Coef2<T, K>& c = coef_at(P.c, it * P.zero);
     const int u = it * NT + tid;
     if (u >= PB * NP) continue;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     const int p = u / NP, i = u - (u / NP) * NP;
     int64_t vx, vy;
     if (!vert(p, vx, vy)) continue;
@@ -760,9 +760,9 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   __syncthreads();
 #pragma unroll 1
   for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
-    const Coef2<T, K>& c = coef_at(P.c, it * P.zero);
     const int u = it * NT + tid;
     if (u >= PB * NP) continue;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     const int p = u / NP, j = u - (u / NP) * NP;
     int64_t vx, vy;
     if (!vert(p, vx, vy)) continue;
@@ -794,9 +794,9 @@ __global__ void __launch_bounds__(256, 2) mvs2d_kernel(const __grid_constant__ M
   __syncthreads();
 #pragma unroll 1
   for (int it = 0; it < cdiv(PB * NP, NT); ++it, ++round) {
-    const Coef2<T, K>& c = coef_at(P.c, it * P.zero);
     const int u = it * NT + tid;
     if (u >= PB * NP) continue;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     const int p = u / NP, i = u - (u / NP) * NP;
     int64_t vx, vy;
     if (!vert(p, vx, vy)) continue;
