@@ -45,6 +45,57 @@ __host__ __device__ constexpr int pick_rb(int lines, int mult, int maxrb) {
   return best;
 }
 
+// Interior rows of all K classes of one cell at once, window index outermost so that every DFMA
+// of an accumulator is separated by the other 3K*RB (or K*RB) accumulators (ILP), coefficients
+// shared by the RB lines.  w[r][o] <-> node (c-2)K + o.
+template <typename T, int K, int RB>
+__device__ __forceinline__ void x_all_interior(const Coef2<T, K>& c, const T (&w)[RB][4 * K + 1], T (&ob)[K][RB],
+                                               T (&ol)[K][RB], T (&om)[K][RB]) {
+#pragma unroll
+  for (int p = 0; p < K; ++p)
+#pragma unroll
+    for (int r = 0; r < RB; ++r) ob[p][r] = ol[p][r] = om[p][r] = 0;
+#pragma unroll
+  for (int o = 0; o <= 4 * K; ++o)
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      const int q = o - p;                           // B coefficient index (offset q - 2K)
+      if (q >= 0 && q <= 4 * K && (p == 0 || (q >= K - p && q <= 4 * K - p))) {
+        const T cb = c.BI[p][q];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) ob[p][r] = fma(cb, w[r][o], ob[p][r]);
+      }
+      const int qm = o - p - K;                      // M/L coefficient index (offset qm - K)
+      if (qm >= 0 && qm <= 2 * K && (p == 0 || (qm >= K - p && qm <= 2 * K - p))) {
+        const T cl = c.LI[p][qm], cm = c.MI[p][qm];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          ol[p][r] = fma(cl, w[r][o], ol[p][r]);
+          om[p][r] = fma(cm, w[r][o], om[p][r]);
+        }
+      }
+    }
+}
+
+// acc[p][r] += sum over the band of class p: WHICH 0 = B (window 4K+1, base (c-2)K), 1 = M, 2 = L
+// (window 2K+1, base (c-1)K); window index outermost.
+template <typename T, int K, int RB, int WHICH, int W>
+__device__ __forceinline__ void y_all_interior(const Coef2<T, K>& c, const T (&w)[RB][W], T (&acc)[K][RB]) {
+#pragma unroll
+  for (int o = 0; o < W; ++o)
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      const int q = o - p;
+      const bool ok = (WHICH == 0) ? (q >= 0 && q <= 4 * K && (p == 0 || (q >= K - p && q <= 4 * K - p)))
+                                   : (q >= 0 && q <= 2 * K && (p == 0 || (q >= K - p && q <= 2 * K - p)));
+      if (ok) {
+        const T cq = (WHICH == 0) ? c.BI[p][q] : (WHICH == 1 ? c.MI[p][q] : c.LI[p][q]);
+#pragma unroll
+        for (int r = 0; r < RB; ++r) acc[p][r] = fma(cq, w[r][o], acc[p][r]);
+      }
+    }
+}
+
 // ----------------------------------------------------------------------------- apply2d
 template <typename T, int K>
 struct ApplyLayout {
@@ -119,6 +170,22 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
         for (int q = 0; q <= 4 * K; ++q) w[r][q] = xb[row * PX + ci * K + q];
       }
       const bool inner = IN || (cx >= 2 && cx <= N - 2);
+      if (inner) {
+        T ob[K][RB], ol[K][RB], om[K][RB];
+        x_all_interior<T, K, RB>(c, w, ob, ol, om);
+#pragma unroll
+        for (int p = 0; p < K; ++p)
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            const int row = g + r * GX;
+            if (row < BW) {
+              sB[row * PO + ci * K + p] = ob[p][r];
+              sL[row * PO + ci * K + p] = ol[p][r];
+              sM[row * PO + ci * K + p] = om[p][r];
+            }
+          }
+        continue;
+      }
 #pragma unroll
       for (int p = 0; p < K; ++p) {
         T ob[RB], ol[RB], om[RB];
@@ -170,6 +237,41 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
       int col[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) col[r] = min(g + r * GY, O - 1);
+      if (inner) {
+        T accL[K][RB];
+#pragma unroll
+        for (int p = 0; p < K; ++p)
+#pragma unroll
+          for (int r = 0; r < RB; ++r) accL[p][r] = 0;
+        {
+          T w[RB][4 * K + 1];
+#pragma unroll
+          for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int q = 0; q <= 4 * K; ++q) w[r][q] = sM[(ci * K + q) * PO + col[r]];
+          y_all_interior<T, K, RB, 0, 4 * K + 1>(c, w, acc);
+        }
+        {
+          T w[RB][2 * K + 1];
+#pragma unroll
+          for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int q = 0; q <= 2 * K; ++q) w[r][q] = sB[(ci * K + K + q) * PO + col[r]];
+          y_all_interior<T, K, RB, 1, 2 * K + 1>(c, w, acc);
+        }
+        {
+          T w[RB][2 * K + 1];
+#pragma unroll
+          for (int r = 0; r < RB; ++r)
+#pragma unroll
+            for (int q = 0; q <= 2 * K; ++q) w[r][q] = sL[(ci * K + K + q) * PO + col[r]];
+          y_all_interior<T, K, RB, 2, 2 * K + 1>(c, w, accL);
+        }
+#pragma unroll
+        for (int p = 0; p < K; ++p)
+#pragma unroll
+          for (int r = 0; r < RB; ++r) acc[p][r] = fma(T(2), accL[p][r], acc[p][r]);
+      } else {
       {
         T w[RB][4 * K + 1];
 #pragma unroll
@@ -214,6 +316,7 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
           for (int r = 0; r < RB; ++r) acc[p][r] += (pass == 0 ? T(1) : T(2)) * tmp[r];
         }
       }
+      }
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
         const int cc = g + r * GY;
@@ -240,18 +343,20 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
 // z[r][i] = sum_l S[l][i] w[r][l]   (S^T w) for RB lines
 template <typename T, int K, int V, int RB>
 __device__ __forceinline__ void s_t(const Coef2<T, K>& c, const T (&w)[RB][2 * K - 1], T (&z)[RB][2 * K - 1]) {
+  // contraction index outermost: NP * RB independent accumulators between dependent FMAs
   constexpr int NP = 2 * K - 1;
 #pragma unroll
-  for (int i = 0; i < NP; ++i) {
+  for (int i = 0; i < NP; ++i)
 #pragma unroll
     for (int r = 0; r < RB; ++r) z[r][i] = 0;
 #pragma unroll
-    for (int l = 0; l < NP; ++l) {
+  for (int l = 0; l < NP; ++l)
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
       const T s = c.S[V][l * NP + i];
 #pragma unroll
       for (int r = 0; r < RB; ++r) z[r][i] = fma(s, w[r][l], z[r][i]);
     }
-  }
 }
 
 // out[r][p] += sum_i S[OFF + p][i] z[r][i] for p in [P0, K)
@@ -259,9 +364,9 @@ template <typename T, int K, int V, int OFF, int P0, int RB>
 __device__ __forceinline__ void s_rows(const Coef2<T, K>& c, const T (&z)[RB][2 * K - 1], T (&out)[RB][K]) {
   constexpr int NP = 2 * K - 1;
 #pragma unroll
-  for (int p = P0; p < K; ++p)
+  for (int i = 0; i < NP; ++i)
 #pragma unroll
-    for (int i = 0; i < NP; ++i) {
+    for (int p = P0; p < K; ++p) {
       const T s = c.S[V][(OFF + p) * NP + i];
 #pragma unroll
       for (int r = 0; r < RB; ++r) out[r][p] = fma(s, z[r][i], out[r][p]);
