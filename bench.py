@@ -162,23 +162,25 @@ def max_over_ranks(v, world):
     return float(t.item())
 
 
-def cpu_oracle_sample(k, seconds_target=15.0):
-    """Time the CPU oracle (as it stands) on an oracle-size twin of the workload: 2D, same k,
-    ~0.26-1M DoFs, one AVS step (CSR residual + dense surrogate patch solves).  Assembly excluded."""
+def cpu_oracle_sample(k, seconds_target=15.0, d=2):
+    """Time the CPU oracle (as it stands) on an oracle-size twin of the workload: same d and k,
+    ~0.26M DoFs (2D) / ~0.06-0.1M DoFs (3D), one AVS step (CSR residual + dense surrogate patch
+    solves).  Assembly excluded."""
     import numpy as np
     from oracle.operator import assemble
     from oracle.smoothers import PatchSolvers, avs_step
     from oracle.discretization import default_sigma
-    N = {2: 256, 3: 170, 4: 128, 5: 102, 6: 85, 7: 73}[k]
+    N = ({2: 256, 3: 170, 4: 128, 5: 102, 6: 85, 7: 73} if d == 2 else {2: 20, 3: 14, 4: 10, 5: 8})[k]
+    omega = 0.25 if d == 2 else 0.1
     s = default_sigma(k)
-    A = assemble(k, 2, N, s)
-    ps = PatchSolvers(k, 2, N, s)
-    x, b = random_xb(k, 2, N)
+    A = assemble(k, d, N, s)
+    ps = PatchSolvers(k, d, N, s)
+    x, b = random_xb(k, d, N)
     ndofs = len(x)
     reps, t_total = 0, 0.0
     while t_total < seconds_target and reps < 50:
         t0 = time.perf_counter()
-        avs_step(A, ps, x, b, 0.25)
+        avs_step(A, ps, x, b, omega)
         t_total += time.perf_counter() - t0
         reps += 1
     try:
@@ -187,7 +189,7 @@ def cpu_oracle_sample(k, seconds_target=15.0):
     except Exception:
         cores = os.cpu_count()
     return {"value": ndofs * reps / t_total / 1e9, "unit": "GDoF/s", "cores": cores, "kind": "oracle",
-            "sample": f"2D k={k} N={N} ({ndofs} DoFs), {reps} AVS step(s) in {t_total:.1f}s, CSR assembly excluded",
+            "sample": f"{d}D k={k} N={N} ({ndofs} DoFs), {reps} AVS step(s) in {t_total:.1f}s, CSR assembly excluded",
             "host_cpus": os.cpu_count()}
 
 
@@ -197,44 +199,49 @@ def run_reference(args):
     if world > 1 and rank != 0:
         return
     k = args.degree
-    cb = cpu_oracle_sample(k, seconds_target=max(5.0, 20.0 / max(1, args.steps + args.warmup)))
+    d = args.dim
+    cb = cpu_oracle_sample(k, seconds_target=max(5.0, 20.0 / max(1, args.steps + args.warmup)), d=d)
     line = {"metric": METRIC, "value": cb["value"], "unit": "GDoF/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg2: 2D unit square Q{k} C0IP, one AVS smoothing step (oracle-size twin)",
-                       "degree": k},
+            "config": {"workload": (f"cfg2: 2D unit square" if d == 2 else f"cfg4: 3D unit cube") +
+                                   f" Q{k} C0IP, one AVS smoothing step (oracle-size twin)", "degree": k, "dim": d},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
 def run_slabs(args, world, rank, local):
-    """Weak scaling over `world` GPUs: global 2D mesh of N = round(N_k sqrt(world)) cells per axis cut into
-    slabs along y; per step every rank exchanges its 4k-2 ghost rows with its neighbours
-    (NCCL send/recv through torch.distributed) and runs the slab smoothing step on its owned rows."""
+    """Weak scaling over `world` GPUs: global mesh of N = round(N_1 world^(1/d)) cells per axis cut into
+    slabs along the slowest axis (y in 2D, z in 3D); per step every rank exchanges its
+    4k-2 ghost rows (planes) with its neighbours (NCCL send/recv through torch.distributed) and runs the
+    slab smoothing step on its owned rows.  N_1: cfg2 (2D); cfg5 N = 128 for k = 3, cfg4 otherwise (3D)."""
     import math
     import torch
     import torch.distributed as dist
     from paper_2412_05082_b200 import api
     from paper_2412_05082_b200.dist import partition, exchange_ghosts
-    k = args.degree
-    N = int(round(CFG2_CELLS[k] * math.sqrt(world)))
+    k, d = args.degree, args.dim
+    N1 = CFG2_CELLS[k] if d == 2 else (128 if k == 3 else CFG4_CELLS[k])
+    N = int(round(N1 * world ** (1.0 / d)))
     dt = torch.float64 if args.dtype == "f64" else torch.float32
     esz = 8 if dt == torch.float64 else 4
-    ctx = api.Context(2, k, 3, cells_override=N, device=local)
+    omega = 0.25 if d == 2 else 0.1
+    ctx = api.Context(d, k, 3, cells_override=N, device=local)
     L = 3
     n = k * N - 1
+    row = n ** (d - 1)
     ga, _ = ctx.slab_ghosts()
     s = partition(N, k, world, ga)[rank]
     rng = torch.Generator(device="cpu").manual_seed(20241205 + rank)
-    xw = (torch.rand(s.lrows * n, generator=rng, dtype=torch.float64) * 2 - 1).to("cuda", dt)
-    bw = (torch.rand(s.lrows * n, generator=rng, dtype=torch.float64) * 2 - 1).to("cuda", dt)
+    xw = (torch.rand(s.lrows * row, generator=rng, dtype=torch.float64) * 2 - 1).to("cuda", dt)
+    bw = (torch.rand(s.lrows * row, generator=rng, dtype=torch.float64) * 2 - 1).to("cuda", dt)
     rw = torch.empty_like(xw)
     stream = torch.cuda.current_stream()
 
     def step():
-        exchange_ghosts(xw, s, n)
-        ctx.slab_avs_step(L, 0.25, s.row0, s.lrows, s.own_lo, s.own_hi, bw, xw, rw)
+        exchange_ghosts(xw, s, row)
+        ctx.slab_avs_step(L, omega, s.row0, s.lrows, s.own_lo, s.own_hi, bw, xw, rw)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -253,18 +260,18 @@ def run_slabs(args, world, rank, local):
     t_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
     launches = ctx.launch_count() - lc0
     own_rows = s.own_hi - s.own_lo
-    total_dofs = n * n
+    total_dofs = n ** d
 
     # e2e: owned rows of x, b from pinned host memory each step, owned x' back
-    xh = xw.view(-1, n)[s.own_local].cpu().contiguous().pin_memory()
-    bh = bw.view(-1, n)[s.own_local].cpu().contiguous().pin_memory()
+    xh = xw.view(-1, row)[s.own_local].cpu().contiguous().pin_memory()
+    bh = bw.view(-1, row)[s.own_local].cpu().contiguous().pin_memory()
     oh = torch.empty_like(xh).pin_memory()
 
     def e2e_step():
-        xw.view(-1, n)[s.own_local].copy_(xh, non_blocking=True)
-        bw.view(-1, n)[s.own_local].copy_(bh, non_blocking=True)
+        xw.view(-1, row)[s.own_local].copy_(xh, non_blocking=True)
+        bw.view(-1, row)[s.own_local].copy_(bh, non_blocking=True)
         step()
-        oh.copy_(xw.view(-1, n)[s.own_local], non_blocking=True)
+        oh.copy_(xw.view(-1, row)[s.own_local], non_blocking=True)
 
     for _ in range(2):
         e2e_step()
@@ -280,14 +287,17 @@ def run_slabs(args, world, rank, local):
         "metric": METRIC, "value": round(total_dofs / (t_ms * 1e-3) / 1e9, 3), "unit": "GDoF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_ms, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": f"cfg2 weak-scaled: 2D unit square, Q{k} C0IP, N={N} cells/axis ({total_dofs} DoFs, "
-                               f"~{total_dofs // world} per GPU), one additive smoothing step per rank on a y-slab "
-                               f"with {ga} NCCL-exchanged ghost rows per side",
+        "config": {"workload": (f"cfg2 weak-scaled: 2D unit square" if d == 2 else
+                                 f"cfg5 weak-scaled: 3D unit cube") +
+                               f", Q{k} C0IP, N={N} cells/axis ({total_dofs} DoFs, "
+                               f"~{total_dofs // world} per GPU), one additive smoothing step (omega={omega}) per rank "
+                               f"on a {'y' if d == 2 else 'z'}-slab with {ga} NCCL-exchanged ghost "
+                               f"{'rows' if d == 2 else 'planes'} per side",
                    "degree": k, "cells": N, "parallelism": f"slab{world}", "ghost_rows": ga,
                    "l2": "inputs larger than L2"},
         "gpu_launches": int(launches), "clocks": clk.summary(),
         "e2e": {"value": round(total_dofs / (t_e2e * 1e-3) / 1e9, 3), "unit": "GDoF/s",
-                "h2d_bytes_per_step": 2 * own_rows * n * esz, "d2h_bytes_per_step": own_rows * n * esz},
+                "h2d_bytes_per_step": 2 * own_rows * row * esz, "d2h_bytes_per_step": own_rows * row * esz},
     }
     if rank == 0:
         print(json.dumps(line))
@@ -503,8 +513,8 @@ def main():
     else:
         ctx.close()
 
-    if rank == 0 and world == 1 and not args.no_cpu and d == 2:
-        line["cpu_baseline"] = cpu_oracle_sample(k)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_oracle_sample(k, d=d)
     if rank == 0:
         print(json.dumps(line))
     if world > 1:

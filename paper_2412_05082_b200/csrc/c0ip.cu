@@ -337,10 +337,11 @@ void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, b
         c0ip::fused_avs<T>(*L.fused, omega, b, x, t.sres.p, st, &ctx->launches))
       continue;
     apply_op<T>(ctx, L, x, b, t.sres.p, st);                     // one residual per AVS step
+    if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
+        c0ip::fused3_fdm_window<T>(*L.fused, omega, t.sres.p, x, sm == C0IP_AVS_ATOMIC, st, &ctx->launches))
+      continue;
     if (sm == C0IP_AVS_ATOMIC) {
-      if (!(ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
-            c0ip::fused3_patch_fdm<T>(*L.fused, omega, t.sres.p, x, nullptr, L.npatch, st, &ctx->launches, 1)))
-        patch_solve<T>(ctx, L, t.sres.p, x, omega, nullptr, L.npatch, 1, st);
+      patch_solve<T>(ctx, L, t.sres.p, x, omega, nullptr, L.npatch, 1, st);
     } else {   // coloured / deterministic generic: serialise writes over the 2^d parity classes
       for (int c = 0; c < (1 << d); ++c) {
         int64_t cnt = L.parity_off[c + 1] - L.parity_off[c];
@@ -353,6 +354,9 @@ void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, b
 // fine += P coarse  (P = E (x) E (x) E, natural embedding)
 template <typename T>
 void prolongate_add_impl(c0ip_ctx ctx, Level& F, const T* coarse, T* fine, cudaStream_t st) {
+  if (ctx->path == C0IP_PATH_AUTO && ctx->d == 2 &&
+      c0ip::fused_transfer2d<T>(ctx->k, true, F.N / 2, coarse, fine, st, &ctx->launches))
+    return;
   Tables<T>& t = tab<T>(F);
   ensure_tmp<T>(F, ctx->d);
   const int64_t nf = F.n, nc = F.E.cols;
@@ -383,6 +387,9 @@ void prolongate_add_impl(c0ip_ctx ctx, Level& F, const T* coarse, T* fine, cudaS
 // coarse = P^T fine (restriction = transpose of the embedding)
 template <typename T>
 void restrict_impl(c0ip_ctx ctx, Level& F, const T* fine, T* coarse, cudaStream_t st) {
+  if (ctx->path == C0IP_PATH_AUTO && ctx->d == 2 &&
+      c0ip::fused_transfer2d<T>(ctx->k, false, F.N / 2, fine, coarse, st, &ctx->launches))
+    return;
   Tables<T>& t = tab<T>(F);
   ensure_tmp<T>(F, ctx->d);
   const int64_t nf = F.n, nc = F.E.cols;
@@ -915,6 +922,31 @@ c0ip_status c0ip_slab_ghosts(c0ip_ctx ctx, int32_t* ghost_avs, int32_t* ghost_ap
   return C0IP_OK;
 }
 
+}  // extern "C"
+
+template <typename T>
+static void slab_apply_impl(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, const c0ip::SlabWindow& w,
+                            cudaStream_t st) {
+  if (c0ip::fused_dim(*L.fused) == 3)
+    c0ip::fused3_apply<T>(*L.fused, x, b, y, st, &ctx->launches, &w);
+  else
+    c0ip::fused_apply<T>(*L.fused, x, b, y, st, &ctx->launches, &w);
+}
+
+// r = b - A x on the rows the owned patches read (wr), then the owned rows of x += omega sum_v R_v^T u_v
+// (2D: gather-form FDM, 3D: parity-class patch FDM restricted to the owned planes; both deterministic)
+template <typename T>
+static void slab_avs(c0ip_ctx ctx, Level& L, T omega, const c0ip::SlabWindow& wr, const c0ip::SlabWindow& wo,
+                     const T* b, T* x, T* r, cudaStream_t st) {
+  slab_apply_impl<T>(ctx, L, x, b, r, wr, st);
+  if (c0ip::fused_dim(*L.fused) == 3)
+    c0ip::fused3_fdm_window<T>(*L.fused, omega, r, x, false, st, &ctx->launches, &wo);
+  else
+    c0ip::fused_fdm<T>(*L.fused, omega, r, x, st, &ctx->launches, &wo);
+}
+
+extern "C" {
+
 static c0ip_status check_window(c0ip_ctx ctx, Level& L, int64_t row0, int64_t lrows, int64_t out_lo,
                                 int64_t out_hi, int64_t ghost) {
   const int64_t KN = int64_t(ctx->k) * L.N;
@@ -925,7 +957,7 @@ static c0ip_status check_window(c0ip_ctx ctx, Level& L, int64_t row0, int64_t lr
     return fail(C0IP_ERR_ARG, "slab window lacks ghost rows (need node rows [" + std::to_string(need_lo) + ", " +
                                   std::to_string(need_hi) + "])");
   if (!L.fused || !c0ip::fused_supports_slab(*L.fused))
-    return fail(C0IP_ERR_STATE, "slab calls need a fused (2D, N >= 8) level");
+    return fail(C0IP_ERR_STATE, "slab calls need a fused level (2D: N >= 8, k <= 7; 3D: N >= 8, k <= 5)");
   return C0IP_OK;
 }
 
@@ -942,15 +974,11 @@ c0ip_status c0ip_slab_avs_step(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, doubl
   const int64_t KN = int64_t(ctx->k) * L.N, gr = 2 * ctx->k - 2;
   c0ip::SlabWindow wr{row0, lrows, std::max<int64_t>(1, out_lo - gr), std::min<int64_t>(KN, out_hi + gr)};
   c0ip::SlabWindow wo{row0, lrows, out_lo, out_hi};
-  if (dt == C0IP_F64) {
-    c0ip::fused_apply<double>(*L.fused, (const double*)x_ext, (const double*)b_ext, (double*)r_ext, st, &ctx->launches, &wr);
-    c0ip::fused_fdm<double>(*L.fused, omega, (const double*)r_ext, (double*)x_ext, st, &ctx->launches, &wo);
-  } else if (dt == C0IP_F32) {
-    c0ip::fused_apply<float>(*L.fused, (const float*)x_ext, (const float*)b_ext, (float*)r_ext, st, &ctx->launches, &wr);
-    c0ip::fused_fdm<float>(*L.fused, (float)omega, (const float*)r_ext, (float*)x_ext, st, &ctx->launches, &wo);
-  } else {
-    return fail(C0IP_ERR_ARG, "bad dtype");
-  }
+  if (dt != C0IP_F64 && dt != C0IP_F32) return fail(C0IP_ERR_ARG, "bad dtype");
+  if (dt == C0IP_F64)
+    slab_avs<double>(ctx, L, omega, wr, wo, (const double*)b_ext, (double*)x_ext, (double*)r_ext, st);
+  else
+    slab_avs<float>(ctx, L, (float)omega, wr, wo, (const float*)b_ext, (float*)x_ext, (float*)r_ext, st);
   return C0IP_OK;
   ABI_CATCH
 }
@@ -966,9 +994,9 @@ c0ip_status c0ip_slab_apply(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, int64_t 
   cudaStream_t st = (cudaStream_t)stream;
   c0ip::SlabWindow w{row0, lrows, out_lo, out_hi};
   if (dt == C0IP_F64)
-    c0ip::fused_apply<double>(*L.fused, (const double*)x_ext, (const double*)b_ext, (double*)y_ext, st, &ctx->launches, &w);
+    slab_apply_impl<double>(ctx, L, (const double*)x_ext, (const double*)b_ext, (double*)y_ext, w, st);
   else if (dt == C0IP_F32)
-    c0ip::fused_apply<float>(*L.fused, (const float*)x_ext, (const float*)b_ext, (float*)y_ext, st, &ctx->launches, &w);
+    slab_apply_impl<float>(ctx, L, (const float*)x_ext, (const float*)b_ext, (float*)y_ext, w, st);
   else
     return fail(C0IP_ERR_ARG, "bad dtype");
   return C0IP_OK;

@@ -39,6 +39,9 @@ struct Apply3P {
   const T* b;
   T* y;
   int64_t N, n;
+  int64_t row0, lrows;      // slab window along z (see SlabWindow); the full domain: 0, n
+  int64_t out_lo, out_hi;   // node planes written
+  int64_t cz_lo, cz_hi;     // cell layers covering [out_lo, out_hi)
   T scale;                  // h^-1
   int zero;
 };
@@ -69,19 +72,21 @@ __device__ __forceinline__ T row_band(F coef, const T* w, int base) {
 }
 
 // K node planes z0 .. z0+K-1 of the in-plane box into smem (cp.async, zero fill outside the domain)
+// (node plane jz lives at local plane jz - 1 - row0, valid for local planes [0, lrows))
 template <typename T, int K, int BW, int PX>
 __device__ __forceinline__ void load_planes_async(T* dst, const T* src, int64_t n, int64_t KN, int64_t z0,
-                                                  int64_t Y0, int64_t X0) {
-  const bool inner = (X0 >= 1 && X0 + BW - 1 <= KN - 1 && Y0 >= 1 && Y0 + BW - 1 <= KN - 1 && z0 >= 1 &&
-                      z0 + K - 1 <= KN - 1);
-  const T* base = src + ((z0 - 1) * n + (Y0 - 1)) * n + (X0 - 1);
+                                                  int64_t Y0, int64_t X0, int64_t row0, int64_t lrows) {
+  const int64_t zlo = (row0 + 1 > 1) ? row0 + 1 : int64_t(1), zhi = (row0 + lrows < KN - 1) ? row0 + lrows : KN - 1;
+  const bool inner = (X0 >= 1 && X0 + BW - 1 <= KN - 1 && Y0 >= 1 && Y0 + BW - 1 <= KN - 1 && z0 >= zlo &&
+                      z0 + K - 1 <= zhi);
+  const T* base = src + ((z0 - 1 - row0) * n + (Y0 - 1)) * n + (X0 - 1);
   for (int e = threadIdx.x; e < K * BW * BW; e += blockDim.x) {
     const int pz = e / (BW * BW), rem = e - pz * (BW * BW), r = rem / BW, cc = rem - (rem / BW) * BW;
     const int64_t off = ((int64_t)pz * n + r) * n + cc;
     bool ok = inner;
     if (!inner) {
       const int64_t jz = z0 + pz, jy = Y0 + r, jx = X0 + cc;
-      ok = (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1 && jz >= 1 && jz <= KN - 1);
+      ok = (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1 && jz >= zlo && jz <= zhi);
     }
     cp_async_elem(dst + (pz * BW + r) * PX + cc, ok ? base + off : src, ok);
   }
@@ -100,7 +105,7 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
   const int64_t N = P.N, n = P.n, KN = K * N;
   const int ntx = int((N + C - 1) / C);
   const int tile = blockIdx.x % (ntx * ntx), chunk = blockIdx.x / (ntx * ntx);
-  const int64_t cx0 = int64_t(tile % ntx) * C, cy0 = int64_t(tile / ntx) * C, cz0 = int64_t(chunk) * CZ;
+  const int64_t cx0 = int64_t(tile % ntx) * C, cy0 = int64_t(tile / ntx) * C, cz0 = P.cz_lo + int64_t(chunk) * CZ;
   const int tid = threadIdx.x;
   const int oy = tid / O, ox = tid - (tid / O) * O;       // z-stage ownership (tid < O*O)
   const bool zown = tid < O * O;
@@ -110,16 +115,16 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
 #pragma unroll
   for (int i = 0; i <= 3 * K; ++i) wP[i] = wQ[i] = 0;
   int round = 0;
-  const int nsteps = int(std::min<int64_t>(CZ, N - cz0)) + 4;
+  const int nsteps = int(std::min<int64_t>(CZ, P.cz_hi - cz0)) + 4;
 
   // prefetch pipeline: the K planes of step s + 1 load while step s computes
-  load_planes_async<T, K, BW, PX>(xb0, P.x, n, KN, (cz0 - 3) * K + 1, (cy0 - 2) * K, (cx0 - 2) * K);
+  load_planes_async<T, K, BW, PX>(xb0, P.x, n, KN, (cz0 - 3) * K + 1, (cy0 - 2) * K, (cx0 - 2) * K, P.row0, P.lrows);
   cp_async_commit();
   for (int s = 0; s < nsteps; ++s) {
     // node planes of this step: (cz0 - 3 + s) K + 1 + pz, pz < K
     if (s + 1 < nsteps)
       load_planes_async<T, K, BW, PX>(xb0 + ((s + 1) & 1) * LY::XB, P.x, n, KN, (cz0 - 2 + s) * K + 1,
-                                      (cy0 - 2) * K, (cx0 - 2) * K);
+                                      (cy0 - 2) * K, (cx0 - 2) * K, P.row0, P.lrows);
     cp_async_commit();
     cp_async_wait1();
     __syncthreads();
@@ -235,7 +240,7 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
 #pragma unroll
         for (int p = 0; p < K; ++p) {
           const int64_t jz = cz * K + p;
-          if (jz < 1 || jz > KN - 1) continue;
+          if (jz < P.out_lo || jz >= P.out_hi) continue;
           const int sp = inner ? -1 : special_row<K>(jz, N);
           T v = 0;
           // windows: wR[i] <-> plane (cz-2)K + i ; wP/wQ[i] <-> plane (cz-1)K + i
@@ -250,7 +255,7 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
                   row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MS[sp][q + K]; }, wP, 0) +
                   T(2) * row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LS[sp][q + K]; }, wQ, 0);
           });
-          const int64_t g = ((jz - 1) * n + (jy - 1)) * n + (jx - 1);
+          const int64_t g = ((jz - 1 - P.row0) * n + (jy - 1)) * n + (jx - 1);
           v *= P.scale;
           P.y[g] = P.b ? P.b[g] - v : v;
         }
@@ -266,9 +271,12 @@ struct Fdm3P {
   Coef2<T, K> c;
   const T* r;
   T* x;
-  const int32_t* list;      // patch ids (nullptr: 0..count-1)
+  const int32_t* list;      // patch ids, or nullptr: the box of vertices vlo + vstr * i, i < vcnt (per axis)
   int64_t count;
+  int vlo[3], vcnt[3], vstr;
   int64_t N, n;
+  int64_t row0, lrows;      // slab window along z (see SlabWindow); the full domain: 0, n
+  int64_t out_lo, out_hi;   // node planes written
   T factor;                 // omega h (A~^-1 = h A^~^-1 in 3D)
   int zero;
   int atomic;               // 1: overlapping patches (atomic AVS, red.global.add), 0: disjoint list
@@ -314,16 +322,25 @@ __global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_consta
   T* buf1 = buf0 + PB * NL;
   __shared__ int64_t gbase[PB];       // global index of the patch's first DoF (or -1)
   __shared__ int8_t pvar[PB][3];      // axis variants
+  __shared__ int pjz[PB];             // node plane of the patch's first DoF plane
   const int64_t N = P.N, n = P.n;
   const int tid = threadIdx.x;
   int round = 0;
   if (tid < PB) {
     const int64_t q = (int64_t)blockIdx.x * PB + tid;
     if (q < P.count) {
-      const int pid = P.list ? P.list[q] : (int)q;
-      const int Nm1 = (int)(N - 1);
-      const int vx = 1 + pid % Nm1, vy = 1 + (pid / Nm1) % Nm1, vz = 1 + pid / (Nm1 * Nm1);
-      gbase[tid] = (((int64_t)(vz - 1) * K) * n + (int64_t)(vy - 1) * K) * n + (int64_t)(vx - 1) * K;
+      int vx, vy, vz;
+      if (P.list) {
+        const int pid = P.list[q], Nm1 = (int)(N - 1);
+        vx = 1 + pid % Nm1; vy = 1 + (pid / Nm1) % Nm1; vz = 1 + pid / (Nm1 * Nm1);
+      } else {
+        const int iq = (int)q, ix = iq % P.vcnt[0], rest = iq / P.vcnt[0];
+        vx = P.vlo[0] + P.vstr * ix;
+        vy = P.vlo[1] + P.vstr * (rest % P.vcnt[1]);
+        vz = P.vlo[2] + P.vstr * (rest / P.vcnt[1]);
+      }
+      gbase[tid] = (((int64_t)(vz - 1) * K - P.row0) * n + (int64_t)(vy - 1) * K) * n + (int64_t)(vx - 1) * K;
+      pjz[tid] = (vz - 1) * K + 1;
       pvar[tid][0] = (int8_t)variant_of(vx, N);
       pvar[tid][1] = (int8_t)variant_of(vy, N);
       pvar[tid][2] = (int8_t)variant_of(vz, N);
@@ -332,7 +349,7 @@ __global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_consta
     }
   }
   __syncthreads();
-  // gather R_v r
+  // gather R_v r (every plane of a patch touching the owned planes lies inside the slab window)
   for (int e = tid; e < PB * NL; e += NT) {
     const int p = e / NL, l = e - p * NL;
     const int lx = l % NP, ly = (l / NP) % NP, lz = l / (NP * NP);
@@ -376,21 +393,25 @@ __global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_consta
       __syncthreads();
     }
   }
-  // scatter: x += omega h u  (disjoint patches within one launch: plain read-modify-write)
+  // scatter: x += omega h u  (disjoint patches within one launch: plain read-modify-write), owned planes only
   for (int e = tid; e < PB * NL; e += NT) {
     const int p = e / NL, l = e - p * NL;
     const int64_t g0 = gbase[p];
     if (g0 < 0) continue;
     const int lx = l % NP, ly = (l / NP) % NP, lz = l / (NP * NP);
     const int64_t g = g0 + ((int64_t)lz * n + ly) * n + lx;
+    const int64_t jz = pjz[p] + lz;
+    if (jz < P.out_lo || jz >= P.out_hi) continue;
     if (P.atomic) atomicAdd(P.x + g, P.factor * in[e]);
     else P.x[g] = fma(P.factor, in[e], P.x[g]);
   }
 }
 
 // ----------------------------------------------------------------------------- host side
+static SlabWindow full_window3(const FusedLevel& F) { return SlabWindow{0, F.n, 1, int64_t(F.k) * F.N}; }
+
 template <typename T, int K>
-static void launch_apply3(const FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st) {
+static void launch_apply3(const FusedLevel& F, const T* x, const T* b, T* y, const SlabWindow& w, cudaStream_t st) {
   using LY = Apply3Layout<T, K>;
   const size_t smem = sizeof(T) * size_t(LY::TOTAL);
   static bool attr = false;
@@ -402,15 +423,25 @@ static void launch_apply3(const FusedLevel& F, const T* x, const T* b, T* y, cud
   Apply3P<T, K> p;
   std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
   p.x = x; p.b = b; p.y = y; p.N = F.N; p.n = F.n;
+  p.row0 = w.row0; p.lrows = w.lrows; p.out_lo = w.out_lo; p.out_hi = w.out_hi;
+  p.cz_lo = w.out_lo / K;
+  p.cz_hi = (w.out_hi - 1) / K + 1;
   p.scale = T(1.0 / F.h);
   p.zero = 0;
-  const int64_t ntx = (F.N + LY::C - 1) / LY::C, nch = (F.N + Tile3<K>::CZ - 1) / Tile3<K>::CZ;
+  const int64_t ntx = (F.N + LY::C - 1) / LY::C, nch = (p.cz_hi - p.cz_lo + Tile3<K>::CZ - 1) / Tile3<K>::CZ;
   apply3d_kernel<T, K><<<(unsigned)(ntx * ntx * nch), 256, smem, st>>>(p);
 }
 
+// patch set of one launch: a device list, or an arithmetic box of vertices (vlo + vstr i per axis)
+struct PatchSet3 {
+  const int32_t* list = nullptr;
+  int64_t count = 0;
+  int vlo[3] = {1, 1, 1}, vcnt[3] = {0, 0, 0}, vstr = 1;
+};
+
 template <typename T, int K>
-static void launch_fdm3(const FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
-                        int atomic, cudaStream_t st) {
+static void launch_fdm3(const FusedLevel& F, T omega, const T* r, T* x, const PatchSet3& ps, int atomic,
+                        const SlabWindow& w, cudaStream_t st) {
   using LY = Fdm3Layout<T, K>;
   const size_t smem = sizeof(T) * size_t(LY::TOTAL);
   static bool attr = false;
@@ -421,11 +452,14 @@ static void launch_fdm3(const FusedLevel& F, T omega, const T* r, T* x, const in
   }
   Fdm3P<T, K> p;
   std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
-  p.r = r; p.x = x; p.list = list; p.count = count; p.N = F.N; p.n = F.n;
+  p.r = r; p.x = x; p.list = ps.list; p.count = ps.count; p.N = F.N; p.n = F.n;
+  for (int a = 0; a < 3; ++a) { p.vlo[a] = ps.vlo[a]; p.vcnt[a] = ps.vcnt[a]; }
+  p.vstr = ps.vstr;
+  p.row0 = w.row0; p.lrows = w.lrows; p.out_lo = w.out_lo; p.out_hi = w.out_hi;
   p.factor = T(double(omega) * F.h);
   p.zero = 0;
   p.atomic = atomic;
-  const int64_t grid = (count + LY::PB - 1) / LY::PB;
+  const int64_t grid = (ps.count + LY::PB - 1) / LY::PB;
   patch_fdm3d_kernel<T, K><<<(unsigned)grid, 256, smem, st>>>(p);
 }
 
@@ -435,13 +469,16 @@ static void check3(const char* what) {
 }
 
 template <typename T>
-bool fused3_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches) {
+bool fused3_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches,
+                  const SlabWindow* win) {
   if (F.d != 3) return false;
+  const SlabWindow w = win ? *win : full_window3(F);
+  if (w.out_hi <= w.out_lo) return true;
   switch (F.k) {
-    case 2: launch_apply3<T, 2>(F, x, b, y, st); break;
-    case 3: launch_apply3<T, 3>(F, x, b, y, st); break;
-    case 4: launch_apply3<T, 4>(F, x, b, y, st); break;
-    case 5: launch_apply3<T, 5>(F, x, b, y, st); break;
+    case 2: launch_apply3<T, 2>(F, x, b, y, w, st); break;
+    case 3: launch_apply3<T, 3>(F, x, b, y, w, st); break;
+    case 4: launch_apply3<T, 4>(F, x, b, y, w, st); break;
+    case 5: launch_apply3<T, 5>(F, x, b, y, w, st); break;
     default: return false;
   }
   (*launches)++;
@@ -450,15 +487,14 @@ bool fused3_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, 
 }
 
 template <typename T>
-bool fused3_patch_fdm(FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
-                      cudaStream_t st, int64_t* launches, int atomic) {
-  if (F.d != 3) return false;
-  if (count == 0) return true;
+static bool fdm3_dispatch(FusedLevel& F, T omega, const T* r, T* x, const PatchSet3& ps, int atomic,
+                          const SlabWindow& w, cudaStream_t st, int64_t* launches) {
+  if (ps.count == 0) return true;
   switch (F.k) {
-    case 2: launch_fdm3<T, 2>(F, omega, r, x, list, count, atomic, st); break;
-    case 3: launch_fdm3<T, 3>(F, omega, r, x, list, count, atomic, st); break;
-    case 4: launch_fdm3<T, 4>(F, omega, r, x, list, count, atomic, st); break;
-    case 5: launch_fdm3<T, 5>(F, omega, r, x, list, count, atomic, st); break;
+    case 2: launch_fdm3<T, 2>(F, omega, r, x, ps, atomic, w, st); break;
+    case 3: launch_fdm3<T, 3>(F, omega, r, x, ps, atomic, w, st); break;
+    case 4: launch_fdm3<T, 4>(F, omega, r, x, ps, atomic, w, st); break;
+    case 5: launch_fdm3<T, 5>(F, omega, r, x, ps, atomic, w, st); break;
     default: return false;
   }
   (*launches)++;
@@ -466,11 +502,70 @@ bool fused3_patch_fdm(FusedLevel& F, T omega, const T* r, T* x, const int32_t* l
   return true;
 }
 
-template bool fused3_apply<double>(FusedLevel&, const double*, const double*, double*, cudaStream_t, int64_t*);
-template bool fused3_apply<float>(FusedLevel&, const float*, const float*, float*, cudaStream_t, int64_t*);
+template <typename T>
+bool fused3_patch_fdm(FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
+                      cudaStream_t st, int64_t* launches, int atomic) {
+  if (F.d != 3 || F.k < 2 || F.k > 5) return false;
+  PatchSet3 ps;
+  if (list) {
+    ps.list = list;
+    ps.count = count;
+  } else {                                   // all patches 0..count-1 (count = (N-1)^3)
+    for (int a = 0; a < 3; ++a) ps.vcnt[a] = int(F.N - 1);
+    ps.count = count;
+  }
+  return fdm3_dispatch<T>(F, omega, r, x, ps, atomic, full_window3(F), st, launches);
+}
+
+template <typename T>
+bool fused3_fdm_window(FusedLevel& F, T omega, const T* r, T* x, bool atomic, cudaStream_t st, int64_t* launches,
+                       const SlabWindow* win) {
+  if (F.d != 3 || F.k < 2 || F.k > 5) return false;
+  const SlabWindow w = win ? *win : full_window3(F);
+  if (w.out_hi <= w.out_lo) return true;
+  const int K = F.k, Nm1 = int(F.N - 1);
+  // patches touching node planes [out_lo, out_hi): (v+1)K - 1 >= out_lo and (v-1)K + 1 <= out_hi - 1
+  const int vz_lo = std::max<int>(1, int((w.out_lo + 1) / K) - 1 + ((w.out_lo + 1) % K ? 1 : 0));
+  const int vz_hi = std::min<int>(Nm1, int((w.out_hi - 2) / K) + 1);
+  if (vz_hi < vz_lo) return true;
+  if (atomic) {
+    PatchSet3 ps;
+    ps.vcnt[0] = ps.vcnt[1] = Nm1;
+    ps.vlo[2] = vz_lo;
+    ps.vcnt[2] = vz_hi - vz_lo + 1;
+    ps.count = int64_t(Nm1) * Nm1 * ps.vcnt[2];
+    return fdm3_dispatch<T>(F, omega, r, x, ps, 1, w, st, launches);
+  }
+  // 2^3 parity classes (v_a mod 2), mutually disjoint patches: deterministic plain stores
+  for (int c = 0; c < 8; ++c) {
+    PatchSet3 ps;
+    ps.vstr = 2;
+    const int lo[3] = {1, 1, vz_lo}, hi[3] = {Nm1, Nm1, vz_hi};
+    int64_t cnt = 1;
+    for (int a = 0; a < 3; ++a) {
+      const int par = (c >> a) & 1;
+      int v0 = lo[a] + ((lo[a] & 1) != par ? 1 : 0);
+      ps.vlo[a] = v0;
+      ps.vcnt[a] = v0 > hi[a] ? 0 : (hi[a] - v0) / 2 + 1;
+      cnt *= ps.vcnt[a];
+    }
+    ps.count = cnt;
+    if (!fdm3_dispatch<T>(F, omega, r, x, ps, 0, w, st, launches)) return false;
+  }
+  return true;
+}
+
+template bool fused3_apply<double>(FusedLevel&, const double*, const double*, double*, cudaStream_t, int64_t*,
+                                   const SlabWindow*);
+template bool fused3_apply<float>(FusedLevel&, const float*, const float*, float*, cudaStream_t, int64_t*,
+                                  const SlabWindow*);
 template bool fused3_patch_fdm<double>(FusedLevel&, double, const double*, double*, const int32_t*, int64_t,
                                        cudaStream_t, int64_t*, int);
 template bool fused3_patch_fdm<float>(FusedLevel&, float, const float*, float*, const int32_t*, int64_t,
                                       cudaStream_t, int64_t*, int);
+template bool fused3_fdm_window<double>(FusedLevel&, double, const double*, double*, bool, cudaStream_t, int64_t*,
+                                        const SlabWindow*);
+template bool fused3_fdm_window<float>(FusedLevel&, float, const float*, float*, bool, cudaStream_t, int64_t*,
+                                       const SlabWindow*);
 
 }  // namespace c0ip

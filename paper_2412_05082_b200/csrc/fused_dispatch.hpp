@@ -45,10 +45,21 @@ bool fused_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega,
 // 3D (fused3d.cu): matvec / residual, and the per-patch FDM update x += omega A~_v^{-1} R_v r over a
 // list of mutually disjoint patches (a parity class or a colour)
 template <typename T>
-bool fused3_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches);
+bool fused3_apply(FusedLevel& F, const T* x, const T* b, T* y, cudaStream_t st, int64_t* launches,
+                  const SlabWindow* win = nullptr);
 template <typename T>
 bool fused3_patch_fdm(FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
                       cudaStream_t st, int64_t* launches, int atomic = 0);
+// additive FDM update of every patch touching the owned planes of the window (nullptr: all patches),
+// writes restricted to the owned planes; atomic scatter, or 8 parity-class launches with plain stores
+template <typename T>
+bool fused3_fdm_window(FusedLevel& F, T omega, const T* r, T* x, bool atomic, cudaStream_t st, int64_t* launches,
+                       const SlabWindow* win = nullptr);
 int fused_dim(const FusedLevel& F);
+
+// 2D transfers (transfer2d.cu): prolong = true: fine += P coarse; false: coarse = P^T fine.
+// Nc = coarse cells per axis (>= 4), returns false if not covered.
+template <typename T>
+bool fused_transfer2d(int k, bool prolong, int64_t Nc, const T* src, T* dst, cudaStream_t st, int64_t* launches);
 
 }  // namespace c0ip

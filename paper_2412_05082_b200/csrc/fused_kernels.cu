@@ -1142,7 +1142,7 @@ bool fused_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega,
   return true;
 }
 
-bool fused_supports_slab(const FusedLevel& F) { return F.d == 2; }
+bool fused_supports_slab(const FusedLevel& F) { return F.d == 2 || (F.d == 3 && F.k <= 5); }
 int fused_dim(const FusedLevel& F) { return F.d; }
 
 #define C0IP_INST(T)                                                                                       \

@@ -197,7 +197,8 @@ def test_avs_deterministic_bitwise_reproducible():
 
 
 # ------------------------------------------------------------------------------ transfers
-@pytest.mark.parametrize("d,k,L", [(2, 2, 3), (2, 5, 3), (2, 7, 2), (3, 2, 3), (3, 4, 2)])
+@pytest.mark.parametrize("d,k,L", [(2, 2, 3), (2, 5, 3), (2, 7, 2), (2, 3, 5), (2, 4, 4), (2, 7, 4),
+                                   (3, 2, 3), (3, 4, 2)])
 def test_transfers(d, k, L):
     from paper_2412_05082_b200 import api
     ctx = api.Context(d, k, L)
@@ -295,6 +296,43 @@ def test_slab_step_bitwise_equals_single_domain(k, N, R):
         yout.view(n, n)[s.own_lo - 1:s.own_hi - 1] = yw.view(-1, n)[s.own_local]
     assert torch.equal(out, full)
     assert torch.equal(yout, yfull)
+    ctx.close()
+
+
+@pytest.mark.parametrize("sm", ["avs", "avs_atomic"])
+@pytest.mark.parametrize("k,N,R", [(2, 16, 2), (3, 12, 3), (5, 10, 2), (4, 40, 2)])
+def test_slab_step_3d(k, N, R, sm):
+    """3D z-slabs: apply is bitwise equal to the single-domain apply on the owned planes; the slab AVS
+    step (parity-class FDM restricted to the owned planes) is bitwise equal to the single-domain
+    deterministic step, and within FP64 tolerance of the atomic one."""
+    from paper_2412_05082_b200 import api
+    from paper_2412_05082_b200.dist import partition
+    ctx = api.Context(3, k, 3, cells_override=N)
+    L = 3
+    n = k * N - 1
+    x, b = random_xb(k, 3, N)
+    full = torch.tensor(x, device=DEV)
+    ctx.smooth(L, sm, 1, 0.1, torch.tensor(b, device=DEV), full)
+    yfull = ctx.apply(L, torch.tensor(x, device=DEV))
+    ga, gp = ctx.slab_ghosts()
+    out = torch.empty_like(full)
+    yout = torch.empty_like(full)
+    plane = n * n
+    for s in partition(N, k, R, ga):
+        rows = slice((s.win_lo - 1) * plane, (s.win_hi - 1) * plane)
+        xw = torch.tensor(x[rows], device=DEV)
+        bw = torch.tensor(b[rows], device=DEV)
+        rw = torch.empty_like(xw)
+        ctx.slab_avs_step(L, 0.1, s.row0, s.lrows, s.own_lo, s.own_hi, bw, xw, rw)
+        out.view(n, plane)[s.own_lo - 1:s.own_hi - 1] = xw.view(-1, plane)[s.own_local]
+        yw = torch.empty_like(xw)
+        ctx.slab_apply(L, s.row0, s.lrows, s.own_lo, s.own_hi, torch.tensor(x[rows], device=DEV), yw)
+        yout.view(n, plane)[s.own_lo - 1:s.own_hi - 1] = yw.view(-1, plane)[s.own_local]
+    assert torch.equal(yout, yfull)
+    if sm == "avs":
+        assert torch.equal(out, full)
+    else:
+        assert rel((out - torch.tensor(x, device=DEV)).cpu().numpy(), (full - torch.tensor(x, device=DEV)).cpu().numpy()) <= 1e-13
     ctx.close()
 
 
