@@ -49,6 +49,19 @@ struct FdmP {
   int64_t out_lo, out_hi;
 };
 
+template <typename T, int K>
+struct MvsP {
+  Coef2<T, K> c;
+  T* x;
+  const T* b;
+  const int32_t* list;      // patch ids of the colour
+  int64_t count;
+  int64_t N, n;
+  T scale;                  // h^-2  (A = h^-2 A^)
+  T factor;                 // omega h^2 (A~^-1 = h^2 A^~^-1)
+  int zero;
+};
+
 template <int K>
 struct Tile {
   // cells per tile edge: ~32 owned nodes per axis
@@ -142,20 +155,26 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 template <typename T, int ROWS, int COLS, int PITCH>
 __device__ __forceinline__ void load_box_async(T* dst, const T* src, int64_t n, int64_t KN, int64_t Y0,
                                                int64_t X0, int64_t row0, int64_t lrows) {
+  // one warp per box row, lanes along the row (no per-element index division)
   const int64_t ylo = (row0 + 1 > 1) ? row0 + 1 : int64_t(1), yhi = (row0 + lrows < KN - 1) ? row0 + lrows : KN - 1;
-  const bool inner = (X0 >= 1 && X0 + COLS - 1 <= KN - 1 && Y0 >= ylo && Y0 + ROWS - 1 <= yhi);
+  const bool xin = (X0 >= 1 && X0 + COLS - 1 <= KN - 1);
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const T* base = src + (Y0 - 1 - row0) * n + (X0 - 1);
-  if (inner) {
-    for (int e = threadIdx.x; e < ROWS * COLS; e += blockDim.x) {
-      const int r = e / COLS, c = e - (e / COLS) * COLS;
-      cp_async_elem(dst + r * PITCH + c, base + (int64_t)r * n + c, true);
-    }
-  } else {
-    for (int e = threadIdx.x; e < ROWS * COLS; e += blockDim.x) {
-      const int r = e / COLS, c = e - (e / COLS) * COLS;
-      const int64_t jy = Y0 + r, jx = X0 + c;
-      const bool ok = (jx >= 1 && jx <= KN - 1 && jy >= ylo && jy <= yhi);
-      cp_async_elem(dst + r * PITCH + c, ok ? base + (int64_t)r * n + c : src, ok);
+  for (int r = threadIdx.x >> 5; r < ROWS; r += nw) {
+    const int64_t jy = Y0 + r;
+    const bool rok = (jy >= ylo && jy <= yhi);
+    const T* rowp = base + (int64_t)r * n;
+    T* d = dst + r * PITCH;
+    if (rok && xin) {
+#pragma unroll
+      for (int c = lane; c < COLS; c += 32) cp_async_elem(d + c, rowp + c, true);
+    } else {
+#pragma unroll
+      for (int c = lane; c < COLS; c += 32) {
+        const int64_t jx = X0 + c;
+        const bool ok = rok && jx >= 1 && jx <= KN - 1;
+        cp_async_elem(d + c, ok ? rowp + c : src, ok);
+      }
     }
   }
 }

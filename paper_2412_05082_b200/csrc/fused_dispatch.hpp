@@ -57,6 +57,14 @@ bool fused3_fdm_window(FusedLevel& F, T omega, const T* r, T* x, bool atomic, cu
                        const SlabWindow* win = nullptr);
 int fused_dim(const FusedLevel& F);
 
+// FP64 tensor-core (DMMA) kernels (mma2d.cu); false if the level / degree is not covered
+// (2D, k = 3, 4) or C0IP_NO_MMA is set
+bool mma_enabled();
+bool mma_fdm2d(const FusedLevel& F, double omega, const double* r, double* x, const SlabWindow& w,
+               cudaStream_t st);
+bool mma_mvs2d(const FusedLevel& F, const int32_t* list, int64_t count, double omega, const double* b, double* x,
+               cudaStream_t st);
+
 // 2D transfers (transfer2d.cu): prolong = true: fine += P coarse; false: coarse = P^T fine.
 // Nc = coarse cells per axis (>= 4), returns false if not covered.
 template <typename T>

@@ -673,19 +673,6 @@ __global__ void __launch_bounds__(256, 2) fdm2d_kernel(const __grid_constant__ F
 //   u_v = A~_v^{-1} r_v by FDM (S^T along x and y, divide by lambda_x + lambda_y, S along y and x),
 //   x  += omega u_v on the patch nodes (disjoint within a colour, plain stores).
 template <typename T, int K>
-struct MvsP {
-  Coef2<T, K> c;
-  T* x;
-  const T* b;
-  const int32_t* list;      // patch ids of the colour
-  int64_t count;
-  int64_t N, n;
-  T scale;                  // h^-2  (A = h^-2 A^)
-  T factor;                 // omega h^2 (A~^-1 = h^2 A^~^-1)
-  int zero;
-};
-
-template <typename T, int K>
 struct MvsLayout {
   static constexpr int NP = 2 * K - 1, BX = 4 * K + 1;
   static constexpr int PER = BX * BX + 3 * BX * NP + 2 * NP * NP;   // per patch
@@ -1081,6 +1068,13 @@ bool fused_fdm(FusedLevel& F, T omega, const T* r, T* x, cudaStream_t st, int64_
   if (F.d != 2) return false;
   const SlabWindow w = win ? *win : full_window(F);
   if (w.out_hi <= w.out_lo) return true;
+  if constexpr (std::is_same<T, double>::value) {
+    if (mma_fdm2d(F, double(omega), r, x, w, st)) {
+      (*launches)++;
+      check_launch("fdm2d_mma launch");
+      return true;
+    }
+  }
   switch (F.k) {
     case 2: launch_fdm<T, 2>(F, omega, r, x, w, st); break;
     case 3: launch_fdm<T, 3>(F, omega, r, x, w, st); break;
@@ -1128,6 +1122,13 @@ bool fused_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega,
                      int64_t* launches) {
   if (F.d != 2) return false;
   if (count == 0) return true;
+  if constexpr (std::is_same<T, double>::value) {
+    if (mma_mvs2d(F, list, count, double(omega), b, x, st)) {
+      (*launches)++;
+      check_launch("mvs2d_mma launch");
+      return true;
+    }
+  }
   switch (F.k) {
     case 2: launch_mvs<T, 2>(F, list, count, omega, b, x, st); break;
     case 3: launch_mvs<T, 3>(F, list, count, omega, b, x, st); break;

@@ -185,6 +185,32 @@ def test_mvs_increment(d, k, N, reverse, generic):
     ctx.set_path(False)
 
 
+# sizes spanning several fused tiles (interior fast paths, ragged last tile) of the 2D kernels
+LARGE_2D = [(2, 2, 40), (2, 3, 27), (2, 3, 32), (2, 4, 27), (2, 4, 32), (2, 5, 21), (2, 7, 13)]
+
+
+@pytest.mark.parametrize("sm", ["avs", "mvs"])
+@pytest.mark.parametrize("d,k,N", LARGE_2D)
+def test_smoother_increment_large_2d(d, k, N, sm):
+    ctx, L = ctx_for(d, k, N)
+    A, ps = oracle(d, k, N)
+    x, b = random_xb(k, d, N)
+    om = 0.25 if sm == "avs" else 1.0
+    step = avs_step if sm == "avs" else mvs_step
+    xt = torch.tensor(x, device=DEV)
+    ctx.smooth(L, sm, 1, om, torch.tensor(b, device=DEV), xt)
+    do = step(A, ps, x, b, om) - x
+    assert rel(xt.cpu().numpy() - x, do) <= FP64_TOL, rel(xt.cpu().numpy() - x, do)
+    xi, bi = x.astype(np.float32).astype(np.float64), b.astype(np.float32).astype(np.float64)
+    x32 = torch.tensor(xi, device=DEV, dtype=torch.float32)
+    ctx.smooth(L, sm, 1, om, torch.tensor(bi, device=DEV, dtype=torch.float32), x32)
+    xo32 = step(A, ps, xi, bi, om)
+    xg32 = x32.cpu().numpy().astype(np.float64)
+    dtol = fp32_delta_tol(ps)
+    assert rel(xg32 - xi, xo32 - xi) <= dtol
+    assert rel(xg32, xo32) <= max(FP32_TOL, dtol * np.linalg.norm(xo32 - xi) / np.linalg.norm(xo32))
+
+
 def test_avs_deterministic_bitwise_reproducible():
     ctx, L = ctx_for(2, 4, 8)
     x, b = random_xb(4, 2, 8)
