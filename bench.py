@@ -45,12 +45,29 @@ def peaks():
         return 6650.0, 1965.0, "fallback"
 
 
+def _alu_peaks():
+    """Measured DFMA / FFMA / DMMA throughput on this B200 pool (tools/alu_peaks.cu, committed as
+    profiles/alu_peaks.json), else the unit-count derivation 148 SMs x 64 (FP64) / 128 (FP32) FMA/clk."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "alu_peaks.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
+
+
 def fp64_peak_tflops(mhz):
-    """B200: 148 SMs x 64 FP64 FMA/clk/SM x 2 flop, at the given clock."""
+    """FP64 peak at the given SM clock: measured DFMA rate (= measured DMMA rate) rescaled from the
+    clock it was measured at; fallback 148 x 64 FMA/clk x 2 flop."""
+    p = _alu_peaks()
+    if p:
+        return max(p["dfma_tflops"], p.get("dmma_m8n8k4_tflops", 0.0)) * mhz / p["dfma_sm_mhz"]
     return 148 * 64 * 2 * mhz * 1e6 / 1e12
 
 
 def fp32_peak_tflops(mhz):
+    p = _alu_peaks()
+    if p:
+        return p["ffma_tflops"] * mhz / p["ffma_sm_mhz"]
     return 148 * 128 * 2 * mhz * 1e6 / 1e12
 
 
@@ -72,8 +89,9 @@ def flops_fdm_3d(k):
 
 
 def flops_fdm_2d(k):
+    """per patch 2d (2k-1)^(d+1) MACs (S^T and S along each axis), k^-d patches per DoF."""
     np_ = 2 * k - 1
-    return 2.0 * (np_ * np_ / k + 2.0 * np_ ** 3 / k ** 2 + (2 * k - 1) * np_ / k)
+    return 2.0 * 4 * np_ ** 3 / k ** 2
 
 
 class ClockSampler:
@@ -439,12 +457,13 @@ def main():
     t_fdm_ms = max(t_step_ms - t_res_ms, 1e-9)
     # dominant kernel of the step and its roofline (algorithmic work / live CUDA-event time)
     if d == 2:
-        kern = "fdm2d" if t_fdm_ms >= t_res_ms else "apply2d"
-        flop = (flops_fdm_2d(k) if kern == "fdm2d" else flops_residual_2d(k)) * ndofs
+        fdm_name = "fdm2d_mma" if (k == 4 and args.dtype == "f64" and not os.environ.get("C0IP_NO_MMA")) else "fdm2d"
+        kern = fdm_name if t_fdm_ms >= t_res_ms else "apply2d"
+        flop = (flops_fdm_2d(k) if kern.startswith("fdm2d") else flops_residual_2d(k)) * ndofs
     else:
         kern = "patch_fdm3d" if t_fdm_ms >= t_res_ms else "apply3d"
         flop = (flops_fdm_3d(k) if kern == "patch_fdm3d" else flops_residual_3d(k)) * ndofs
-    t_k = t_fdm_ms if kern in ("fdm2d", "patch_fdm3d") else t_res_ms
+    t_k = t_fdm_ms if kern in ("fdm2d", "fdm2d_mma", "patch_fdm3d") else t_res_ms
     byts = 3 * esz * ndofs
     peak_alu = fp64_peak_tflops(clk_mhz) if esz == 8 else fp32_peak_tflops(clk_mhz)
     ach_tf = flop / (t_k * 1e-3) / 1e12
@@ -460,7 +479,9 @@ def main():
                "frac": round(f_alu, 4)}
     roof["kernel"] = kern
     roof["traffic"] = traffic_from_profiles(f"{kern}_kernel_k{k}_{args.dtype}")
-    roof["peak_source"] = f"hbm {peak_src} (MEASURED_PEAKS.json); alu derived 148x{64 if esz == 8 else 128}x2 flop/clk at {clk_mhz:.0f} MHz (DESIGN.md)"
+    roof["peak_source"] = (f"hbm {peak_src} (MEASURED_PEAKS.json); alu " +
+                           ("measured (profiles/alu_peaks.json, tools/alu_peaks.cu)" if _alu_peaks() else
+                            f"derived 148x{64 if esz == 8 else 128}x2 flop/clk") + f" rescaled to {clk_mhz:.0f} MHz")
     roof["alt"] = alt
     roof["launch_ms"] = round(t_k, 4)
 

@@ -11,6 +11,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/c0ip.h"
@@ -301,6 +302,21 @@ void patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, const int32_
   CK(cudaGetLastError());
 }
 
+// 2D FP64: patch solves on the tensor cores (mma2d.cu)
+template <typename T>
+bool mma_patches(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, const int32_t* list, int64_t count, int atomic,
+                 cudaStream_t st) {
+  if constexpr (std::is_same<T, double>::value) {
+    if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 2 &&
+        c0ip::mma_patch_fdm2d(*L.fused, omega, r, x, list, count, atomic, st)) {
+      ctx->launches++;
+      CK(cudaGetLastError());
+      return true;
+    }
+  }
+  return false;
+}
+
 // x += omega A~_v^{-1} R_v r over disjoint patches (tuned 3D kernel when available, else generic)
 template <typename T>
 void disjoint_patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, const int32_t* list, int64_t count,
@@ -308,6 +324,7 @@ void disjoint_patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, con
   if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
       c0ip::fused3_patch_fdm<T>(*L.fused, omega, r, x, list, count, st, &ctx->launches))
     return;
+  if (mma_patches<T>(ctx, L, r, x, omega, list, count, 0, st)) return;
   patch_solve<T>(ctx, L, r, x, omega, list, count, 0, st);
 }
 
@@ -341,6 +358,7 @@ void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, b
         c0ip::fused3_fdm_window<T>(*L.fused, omega, t.sres.p, x, sm == C0IP_AVS_ATOMIC, st, &ctx->launches))
       continue;
     if (sm == C0IP_AVS_ATOMIC) {
+      if (mma_patches<T>(ctx, L, t.sres.p, x, omega, nullptr, L.npatch, 1, st)) continue;
       patch_solve<T>(ctx, L, t.sres.p, x, omega, nullptr, L.npatch, 1, st);
     } else {   // coloured / deterministic generic: serialise writes over the 2^d parity classes
       for (int c = 0; c < (1 << d); ++c) {

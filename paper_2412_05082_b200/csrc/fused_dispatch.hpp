@@ -62,6 +62,10 @@ int fused_dim(const FusedLevel& F);
 bool mma_enabled();
 bool mma_fdm2d(const FusedLevel& F, double omega, const double* r, double* x, const SlabWindow& w,
                cudaStream_t st);
+// x += omega A~_v^{-1} R_v r over a patch list (nullptr: all patches); atomic: red.global.add (patches
+// may overlap), else plain read-modify-write (the list must be mutually disjoint)
+bool mma_patch_fdm2d(const FusedLevel& F, double omega, const double* r, double* x, const int32_t* list,
+                     int64_t count, int atomic, cudaStream_t st);
 bool mma_mvs2d(const FusedLevel& F, const int32_t* list, int64_t count, double omega, const double* b, double* x,
                cudaStream_t st);
 

@@ -277,13 +277,13 @@ struct MvsMma {
   }
   __host__ __device__ static constexpr bool bm(int b) { return need(-K - 1, 3 * K - 1, b); }   // B^_x band
   __host__ __device__ static constexpr bool bl(int b) { return need(-1, 2 * K - 1, b); }       // L^_x, M^_x band
-  // per-lane fragments of one axis variant (stored in smem for all variants)
-  struct YF {                 // stage Y A fragments: Op_y[jy0 + g][row0 + 4c + q]
-    double m[CML], l[CML], b[CB];
-  };
-  struct XF {                 // stage X B fragments: Op_x[jx0 + g][block + 2q + c] (L pre-multiplied by 2)
-    double bx[3][2], lx[3][2], mx[3][2];
-  };
+  // rows of x loaded: [jy0 - K - 1, jy0 - K - 1 + RL); M^/L^ chunk c starts at row offset K + 4c
+  static constexpr int RL = (K + 4 * CML > 4 * CB) ? K + 4 * CML : 4 * CB;
+  // per-variant constant fragments, structure of arrays over the 32 lanes (conflict-free LDS):
+  //   Y[v][f][lane], f = c (M^_y chunk c), CML + c (L^_y), 2 CML + c (B^_y):  Op_y[jy0 + g][row + q]
+  //   X[v][f][lane] (double2 over c = 0, 1), f = 3 op + block, op 0 B^_x, 1 2 L^_x, 2 M^_x:
+  //                                                                          Op_x[jx0 + g][block + 2q + c]
+  static constexpr int NY = 2 * CML + CB, NX = 9;
 };
 
 // full-band 1D operator coefficient (reference scale) between nodes jo (row) and ji (column):
@@ -306,14 +306,12 @@ __device__ double op1d(const Coef2<double, K>& c, int which, int64_t jo, int64_t
 }
 
 template <int K>
-__global__ void __launch_bounds__(256, 2) mvs2d_mma_kernel(const __grid_constant__ MvsP<double, K> P) {
+__global__ void __launch_bounds__(256, 3) mvs2d_mma_kernel(const __grid_constant__ MvsP<double, K> P) {
   using MV = MvsMma<K>;
-  using YF = typename MV::YF;
-  using XF = typename MV::XF;
-  constexpr int NP = MV::NP, CML = MV::CML, CB = MV::CB;
+  constexpr int NP = MV::NP, CML = MV::CML, CB = MV::CB, NY = MV::NY, NX = MV::NX;
   constexpr int NT = 256;
-  __shared__ YF yfs[3][32];
-  __shared__ XF xfs[3][32];
+  __shared__ double ys[3][NY][32];
+  __shared__ double2 xs[3][NX][32];
   __shared__ Frag ffs[3][32];
   __shared__ double2 sfs[9][32];
   const int64_t N = P.N, n = P.n, KN = K * N;
@@ -321,36 +319,30 @@ __global__ void __launch_bounds__(256, 2) mvs2d_mma_kernel(const __grid_constant
   const int g = lane >> 2, q = lane & 3;
 
   // constant fragments of the three axis variants (left / interior / right: representative vertex
-  // v = 1, N/2, N - 1 -- the interior representative's whole band lies inside the domain), the
-  // interior one kept in registers
+  // v = 1, N/2, N - 1 -- the interior representative's whole band lies inside the domain)
   if (tid < 96) {
-    const int v = tid >> 5, gg = (tid & 31) >> 2, qq = tid & 3;
+    const int v = tid >> 5, gg = (tid & 31) >> 2, qq = tid & 3, l = tid & 31;
     const int64_t vr = v == 0 ? 1 : (v == 1 ? N / 2 : N - 1);
     const int64_t j0 = (vr - 1) * K + 1;                 // first patch node
     const int64_t jo = gg < NP ? j0 + gg : -1;           // padding row: zero fragments
-    YF yf;
     for (int c = 0; c < CML; ++c) {
-      yf.m[c] = op1d<K>(P.c, 1, jo, j0 - 1 + 4 * c + qq, N);
-      yf.l[c] = op1d<K>(P.c, 2, jo, j0 - 1 + 4 * c + qq, N);
+      ys[v][c][l] = op1d<K>(P.c, 1, jo, j0 - 1 + 4 * c + qq, N);
+      ys[v][CML + c][l] = op1d<K>(P.c, 2, jo, j0 - 1 + 4 * c + qq, N);
     }
-    for (int c = 0; c < CB; ++c) yf.b[c] = op1d<K>(P.c, 0, jo, j0 - K - 1 + 4 * c + qq, N);
-    yfs[v][tid & 31] = yf;
-    XF xf;
-    for (int bb = 0; bb < 3; ++bb)
-      for (int c = 0; c < 2; ++c) {
-        const int64_t ji = j0 - 9 + 8 * bb + 2 * qq + c;
-        xf.bx[bb][c] = op1d<K>(P.c, 0, jo, ji, N);
-        xf.lx[bb][c] = 2.0 * op1d<K>(P.c, 2, jo, ji, N);
-        xf.mx[bb][c] = op1d<K>(P.c, 1, jo, ji, N);
-      }
-    xfs[v][tid & 31] = xf;
+    for (int c = 0; c < CB; ++c) ys[v][2 * CML + c][l] = op1d<K>(P.c, 0, jo, j0 - K - 1 + 4 * c + qq, N);
+    for (int bb = 0; bb < 3; ++bb) {
+      const int64_t ji = j0 - 9 + 8 * bb + 2 * qq;
+      xs[v][bb][l] = make_double2(op1d<K>(P.c, 0, jo, ji, N), op1d<K>(P.c, 0, jo, ji + 1, N));
+      xs[v][3 + bb][l] = make_double2(2.0 * op1d<K>(P.c, 2, jo, ji, N), 2.0 * op1d<K>(P.c, 2, jo, ji + 1, N));
+      xs[v][6 + bb][l] = make_double2(op1d<K>(P.c, 1, jo, ji, N), op1d<K>(P.c, 1, jo, ji + 1, N));
+    }
     Frag f;
     for (int c = 0; c < 2; ++c) {
       const int a = 2 * qq + c;
       f.f1[c] = (a < NP && gg < NP) ? P.c.S[v][a * NP + gg] : 0.0;
       f.f2[c] = (a < NP && gg < NP) ? P.c.S[v][gg * NP + a] : 0.0;
     }
-    ffs[v][tid & 31] = f;
+    ffs[v][l] = f;
   }
   for (int e = tid; e < 9 * 32; e += NT) {
     const int vx = e / 96, vy = (e / 32) % 3, l = e & 31;
@@ -361,84 +353,92 @@ __global__ void __launch_bounds__(256, 2) mvs2d_mma_kernel(const __grid_constant
     sfs[vx * 3 + vy][l] = sc;
   }
   __syncthreads();
-  const YF yi = yfs[1][lane];
-  const XF xi = xfs[1][lane];
-  const Frag fi = ffs[1][lane];
-  const double2 si = sfs[4][lane];
-  const int Nm1 = int(N - 1);
+  const int Nm1 = int(N - 1), KNi = int(KN), ni = int(n);
+  const unsigned magic = unsigned(0xFFFFFFFFull / unsigned(Nm1));
   const double* __restrict__ X = P.x;
 
-  auto body = [&](const YF& yf, const XF& xf, const Frag& fx, const Frag& fy, double2 sc, int64_t jx0, int64_t jy0,
-                  bool edge) {
-    // x fragments: rows row0 + 4c + q, column block + g (zero outside the interior nodes)
-    auto ld = [&](int64_t jy, int64_t jx) -> double {
-      if (edge && (jx < 1 || jx > KN - 1 || jy < 1 || jy > KN - 1)) return 0.0;
-      return __ldg(X + (jy - 1) * n + (jx - 1));
+  // one patch: x rows [jy0 - K - 1, + RL), column blocks [jx0 - 9 + 8b, + 8) (lane: row q + 4c, column g)
+  auto body = [&](int vx, int vy, bool edge) {
+    const int jx0 = (vx - 1) * K + 1, jy0 = (vy - 1) * K + 1;
+    const int vary = edge ? (vy == 1 ? 0 : (vy == Nm1 ? 2 : 1)) : 1;
+    const int varx = edge ? (vx == 1 ? 0 : (vx == Nm1 ? 2 : 1)) : 1;
+    const double* base = X + int64_t(jy0 - K - 2) * n + (jx0 - 10);   // node (jy0 - K - 1, jx0 - 9)
+    auto ld = [&](int r, int col) -> double {                          // r, col relative to that node
+      if (edge) {
+        const int jy = jy0 - K - 1 + r, jx = jx0 - 9 + col;
+        if (jx < 1 || jx > KNi - 1 || jy < 1 || jy > KNi - 1) return 0.0;
+      }
+      return __ldg(base + (r * ni + col));
     };
     double xm[3][CML], xb[3][CB];
 #pragma unroll
     for (int bb = 0; bb < 3; ++bb) {
-      const int64_t jx = jx0 - 9 + 8 * bb + g;
-      if (MV::bm(bb) || MV::bl(bb)) {
-#pragma unroll
-        for (int c = 0; c < CML; ++c) xm[bb][c] = ld(jy0 - 1 + 4 * c + q, jx);
-      }
       if (MV::bl(bb)) {
 #pragma unroll
-        for (int c = 0; c < CB; ++c) xb[bb][c] = ld(jy0 - K - 1 + 4 * c + q, jx);
+        for (int c = 0; c < CB; ++c) xb[bb][c] = ld(4 * c + q, 8 * bb + g);
+      }
+      if (MV::bm(bb) || MV::bl(bb)) {
+#pragma unroll
+        for (int c = 0; c < CML; ++c) {
+          // M^/L^ rows start K rows below the B^ rows: for K = 4 they are chunks of the B^ load
+          if (K % 4 == 0 && MV::bl(bb) && c + K / 4 < CB) xm[bb][c] = xb[bb][c + K / 4];
+          else xm[bb][c] = ld(K + 4 * c + q, 8 * bb + g);
+        }
       }
     }
-    double bv0 = 0.0, bv1 = 0.0;
-    const int64_t jy = jy0 + g, jx = jx0 + 2 * q;
+    const int jy = jy0 + g, jx = jx0 + 2 * q;
     const bool r0 = g < NP && 2 * q < NP, r1 = g < NP && 2 * q + 1 < NP;
-    if (r0) bv0 = __ldg(P.b + (jy - 1) * n + (jx - 1));
-    if (r1) bv1 = __ldg(P.b + (jy - 1) * n + jx);
+    const int64_t po = int64_t(jy - 1) * n + (jx - 1);
+    const double bv0 = r0 ? __ldg(P.b + po) : 0.0;
+    const double bv1 = r1 ? __ldg(P.b + po + 1) : 0.0;
     // stage Y then stage X, accumulated into (a0, a1) = [y_out = g][x_out = 2q + s]
+    const double* yv = &ys[vary][0][lane];
+    const double2* xv = &xs[varx][0][lane];
     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
     for (int bb = 0; bb < 3; ++bb) {
       if (MV::bm(bb)) {
         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-        for (int c = 0; c < CML; ++c) dmma(d0, d1, yf.m[c], xm[bb][c], d0, d1);
-        dmma(a0, a1, d0, xf.bx[bb][0], a0, a1);
-        dmma(a0, a1, d1, xf.bx[bb][1], a0, a1);
+        for (int c = 0; c < CML; ++c) dmma(d0, d1, yv[c * 32], xm[bb][c], d0, d1);
+        const double2 f = xv[bb * 32];
+        dmma(a0, a1, d0, f.x, a0, a1);
+        dmma(a0, a1, d1, f.y, a0, a1);
       }
       if (MV::bl(bb)) {
         double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
-        for (int c = 0; c < CML; ++c) dmma(d0, d1, yf.l[c], xm[bb][c], d0, d1);
+        for (int c = 0; c < CML; ++c) dmma(d0, d1, yv[(CML + c) * 32], xm[bb][c], d0, d1);
 #pragma unroll
-        for (int c = 0; c < CB; ++c) dmma(e0, e1, yf.b[c], xb[bb][c], e0, e1);
-        dmma(a0, a1, d0, xf.lx[bb][0], a0, a1);
-        dmma(a0, a1, d1, xf.lx[bb][1], a0, a1);
-        dmma(a0, a1, e0, xf.mx[bb][0], a0, a1);
-        dmma(a0, a1, e1, xf.mx[bb][1], a0, a1);
+        for (int c = 0; c < CB; ++c) dmma(e0, e1, yv[(2 * CML + c) * 32], xb[bb][c], e0, e1);
+        const double2 fl = xv[(3 + bb) * 32], fm = xv[(6 + bb) * 32];
+        dmma(a0, a1, d0, fl.x, a0, a1);
+        dmma(a0, a1, d1, fl.y, a0, a1);
+        dmma(a0, a1, e0, fm.x, a0, a1);
+        dmma(a0, a1, e1, fm.y, a0, a1);
       }
     }
     const double rr0 = fma(-P.scale, a0, bv0), rr1 = fma(-P.scale, a1, bv1);
     double u0, u1;
-    patch_solve(fx, fy, sc, rr0, rr1, u0, u1);
-    double* xp = P.x + (jy - 1) * n + (jx - 1);
+    patch_solve(ffs[varx][lane], ffs[vary][lane], sfs[varx * 3 + vary][lane], rr0, rr1, u0, u1);
+    double* xp = P.x + po;
     if (r0) xp[0] += u0;
     if (r1) xp[1] += u1;
   };
 
+  constexpr int YTOP = MV::RL - K - 2;   // last loaded row relative to jy0
 #pragma unroll 1
   for (int64_t pi = int64_t(blockIdx.x) * (NT / 32) + warp; pi < P.count; pi += int64_t(gridDim.x) * (NT / 32)) {
     const int pid = P.list[pi];
-    const int vx = 1 + pid % Nm1, vy = 1 + pid / Nm1;
-    const int64_t jx0 = int64_t(vx - 1) * K + 1, jy0 = int64_t(vy - 1) * K + 1;
-    // loads stay inside the interior nodes: columns [jx0 - 9, jx0 + 14], rows [jy0 - K - 1, ytop]
-    constexpr int YTOP = (4 * CML - 2 > 4 * CB - K - 2) ? 4 * CML - 2 : 4 * CB - K - 2;
-    const bool safe = jx0 - 9 >= 1 && jx0 + 14 <= KN - 1 && jy0 - K - 1 >= 1 && jy0 + YTOP <= KN - 1;
-    if (safe && vx >= 2 && vx <= Nm1 - 1 && vy >= 2 && vy <= Nm1 - 1) {
-      body(yi, xi, fi, fi, si, jx0, jy0, false);
-    } else {
-      const int varx = vx == 1 ? 0 : (vx == Nm1 ? 2 : 1), vary = vy == 1 ? 0 : (vy == Nm1 ? 2 : 1);
-      body(yfs[vary][lane], xfs[varx][lane], ffs[varx][lane], ffs[vary][lane], sfs[varx * 3 + vary][lane], jx0, jy0,
-           true);
-    }
+    int qy = int(__umulhi(unsigned(pid), magic));        // pid / (N - 1), at most one short
+    if (pid - qy * Nm1 >= Nm1) ++qy;
+    const int vy = 1 + qy, vx = 1 + pid - qy * Nm1;
+    const int jx0 = (vx - 1) * K + 1, jy0 = (vy - 1) * K + 1;
+    // fast path: interior variants on both axes and every loaded node inside the interior
+    const bool fast = vx >= 2 && vx <= Nm1 - 1 && vy >= 2 && vy <= Nm1 - 1 && jx0 - 9 >= 1 && jx0 + 14 <= KNi - 1 &&
+                      jy0 - K - 1 >= 1 && jy0 + YTOP <= KNi - 1;
+    if (fast) body(vx, vy, false);
+    else body(vx, vy, true);
   }
 }
 
@@ -475,6 +475,95 @@ bool mma_mvs2d(const FusedLevel& F, const int32_t* list, int64_t count, double o
   }
 }
 
+// ----------------------------------------------------------------------------- patch_fdm2d_mma
+// x += omega h^2 R_v^T A~_v^{-1} R_v r for a list of patches (nullptr: every patch), one patch per warp:
+// the paper's atomic AVS (fire-and-forget red.global.add.f64) or, for mutually disjoint
+// patches (a parity class: coloured AVS), plain read-modify-write.
+template <int K>
+__global__ void __launch_bounds__(256, 4) patch_fdm2d_mma_kernel(const __grid_constant__ MvsP<double, K> P,
+                                                                 const double* __restrict__ r, int atomic) {
+  constexpr int NP = 2 * K - 1, NT = 256;
+  __shared__ Frag ffs[3][32];
+  __shared__ double2 sfs[9][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  if (tid < 96) {
+    const int v = tid >> 5, gg = (tid & 31) >> 2, qq = tid & 3;
+    Frag f;
+    for (int c = 0; c < 2; ++c) {
+      const int a = 2 * qq + c;
+      f.f1[c] = (a < NP && gg < NP) ? P.c.S[v][a * NP + gg] : 0.0;
+      f.f2[c] = (a < NP && gg < NP) ? P.c.S[v][gg * NP + a] : 0.0;
+    }
+    ffs[v][tid & 31] = f;
+  }
+  for (int e = tid; e < 9 * 32; e += NT) {
+    const int vx = e / 96, vy = (e / 32) % 3, l = e & 31;
+    const int i = l >> 2, j0 = 2 * (l & 3);
+    double2 sc;
+    sc.x = (i < NP && j0 < NP) ? P.factor / (P.c.lam[vx][i] + P.c.lam[vy][j0]) : 0.0;
+    sc.y = (i < NP && j0 + 1 < NP) ? P.factor / (P.c.lam[vx][i] + P.c.lam[vy][j0 + 1]) : 0.0;
+    sfs[vx * 3 + vy][l] = sc;
+  }
+  __syncthreads();
+  const int Nm1 = int(P.N - 1);
+  const unsigned magic = unsigned(0xFFFFFFFFull / unsigned(Nm1));
+  const int64_t n = P.n;
+  const bool r0 = g < NP && 2 * q < NP, r1 = g < NP && 2 * q + 1 < NP;
+#pragma unroll 1
+  for (int64_t pi = int64_t(blockIdx.x) * (NT / 32) + warp; pi < P.count; pi += int64_t(gridDim.x) * (NT / 32)) {
+    const int pid = P.list ? P.list[pi] : int(pi);
+    int qy = int(__umulhi(unsigned(pid), magic));        // pid / (N - 1), at most one short
+    if (pid - qy * Nm1 >= Nm1) ++qy;
+    const int vy = 1 + qy, vx = 1 + pid - qy * Nm1;
+    const int varx = vx == 1 ? 0 : (vx == Nm1 ? 2 : 1), vary = vy == 1 ? 0 : (vy == Nm1 ? 2 : 1);
+    const int64_t po = int64_t((vy - 1) * K + g) * n + (vx - 1) * K + 2 * q;   // node (jy0 + g, jx0 + 2q)
+    const double b0 = r0 ? __ldg(r + po) : 0.0, b1 = r1 ? __ldg(r + po + 1) : 0.0;
+    double u0, u1;
+    patch_solve(ffs[varx][lane], ffs[vary][lane], sfs[varx * 3 + vary][lane], b0, b1, u0, u1);
+    double* xp = P.x + po;
+    if (atomic) {
+      if (r0) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp), "d"(u0) : "memory");
+      if (r1) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp + 1), "d"(u1) : "memory");
+    } else {
+      if (r0) xp[0] += u0;
+      if (r1) xp[1] += u1;
+    }
+  }
+}
+
+template <int K>
+static void launch_patch_fdm_mma(const FusedLevel& F, double omega, const double* r, double* x, const int32_t* list,
+                                 int64_t count, int atomic, cudaStream_t st) {
+  static int grid_cache = -1;
+  if (grid_cache < 0) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, patch_fdm2d_mma_kernel<K>, 256, 0);
+    grid_cache = sms * std::max(per, 1);
+  }
+  MvsP<double, K> p;
+  std::memcpy(&p.c, F.c64.data(), sizeof(p.c));
+  p.x = x; p.b = nullptr; p.list = list; p.count = count; p.N = F.N; p.n = F.n;
+  p.scale = 1.0 / (F.h * F.h);
+  p.factor = omega * F.h * F.h;
+  p.zero = 0;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid_cache, (count + 7) / 8));
+  patch_fdm2d_mma_kernel<K><<<grid, 256, 0, st>>>(p, r, atomic);
+}
+
+bool mma_patch_fdm2d(const FusedLevel& F, double omega, const double* r, double* x, const int32_t* list,
+                     int64_t count, int atomic, cudaStream_t st) {
+  if (!mma_enabled() || F.d != 2 || count <= 0) return false;
+  switch (F.k) {
+    case 2: launch_patch_fdm_mma<2>(F, omega, r, x, list, count, atomic, st); return true;
+    case 3: launch_patch_fdm_mma<3>(F, omega, r, x, list, count, atomic, st); return true;
+    case 4: launch_patch_fdm_mma<4>(F, omega, r, x, list, count, atomic, st); return true;
+    default: return false;
+  }
+}
+
 bool mma_enabled() {
   static const bool on = (std::getenv("C0IP_NO_MMA") == nullptr);
   return on;
@@ -482,8 +571,9 @@ bool mma_enabled() {
 
 bool mma_fdm2d(const FusedLevel& F, double omega, const double* r, double* x, const SlabWindow& w, cudaStream_t st) {
   if (!mma_enabled() || F.d != 2) return false;
+  // k = 4 only: at k = 3 the 5 -> 8 padding makes the DMMA solve slower than fdm2d_kernel (measured
+  // 0.43 vs 0.28 ms at 16.7M DoFs)
   switch (F.k) {
-    case 3: launch_fdm_mma<3>(F, omega, r, x, w, st); return true;
     case 4: launch_fdm_mma<4>(F, omega, r, x, w, st); return true;
     default: return false;
   }

@@ -64,8 +64,11 @@ def main(rep, out, suffix):
                 return v * {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9}.get(u, 1)
             tb = mb('dram__bytes_read.sum') + mb('dram__bytes_write.sum')
             short = name.split('<')[0].split()[-1].replace('c0ip::', '')
-            kk = name.split(',')[1].strip().replace('(int)', '').rstrip('>').split('>')[0] if ',' in name else '?'
-            dt = 'f64' if '<double' in name else 'f32'
+            import re
+            targs = name.split('<', 1)[1].split('>(')[0] if '<' in name else ''
+            ints = re.findall(r'\b(\d+)\b', targs)
+            kk = ints[-1] if ints else '?'
+            dt = 'f64' if ('double' in name or 'mma' in short) else 'f32'
             key = f"{short}_k{kk}_{dt}"
             traffic[key] = tb
             lines.append(f"dram traffic per launch: {tb / 1e6:.1f} MB (key {key})")
