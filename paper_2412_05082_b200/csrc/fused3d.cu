@@ -274,6 +274,7 @@ struct Fdm3P {
   const int32_t* list;      // patch ids, or nullptr: the box of vertices vlo + vstr * i, i < vcnt (per axis)
   int64_t count;
   int vlo[3], vcnt[3], vstr;
+  unsigned mag[2];          // floor((2^32 - 1) / d) for d = vcnt[0], vcnt[1] (list mode: N - 1, (N - 1)^2)
   int64_t N, n;
   int64_t row0, lrows;      // slab window along z (see SlabWindow); the full domain: 0, n
   int64_t out_lo, out_hi;   // node planes written
@@ -282,8 +283,10 @@ struct Fdm3P {
   int atomic;               // 1: overlapping patches (atomic AVS, red.global.add), 0: disjoint list
 };
 
+// CTA-cooperative variant (PB patches per CTA, one thread per patch line, smem gather/scatter): faster
+// than the warp-per-patch kernel for the disjoint parity-class / colour lists (plain stores)
 template <typename T, int K>
-struct Fdm3Layout {
+struct Fdm3CtaLayout {
   static constexpr int NP = 2 * K - 1, NL = NP * NP * NP;
   static constexpr int PB = cdiv(256, NP * NP);   // patches per CTA so that one stage ~ 256 lines
   static constexpr int TOTAL = 2 * PB * NL;
@@ -313,8 +316,8 @@ __device__ __forceinline__ void contract3(const Coef2<T, K>& c, int var, const T
 }
 
 template <typename T, int K>
-__global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_constant__ Fdm3P<T, K> P) {
-  using LY = Fdm3Layout<T, K>;
+__global__ void __launch_bounds__(256, 2) patch_fdm3d_cta_kernel(const __grid_constant__ Fdm3P<T, K> P) {
+  using LY = Fdm3CtaLayout<T, K>;
   constexpr int NP = LY::NP, NL = LY::NL, PB = LY::PB;
   constexpr int NT = 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -407,6 +410,203 @@ __global__ void __launch_bounds__(256, 2) patch_fdm3d_kernel(const __grid_consta
   }
 }
 
+template <typename T, int K>
+struct Fdm3Layout {
+  static constexpr int NP = 2 * K - 1, NL = NP * NP * NP, NL2 = NP * NP;
+  static constexpr int LPL = cdiv(NL2, 32);        // patch lines per lane
+  static constexpr int WB = NL + (NL % 2 == 0 ? 1 : 0);   // per-warp buffer (odd pitch)
+  static constexpr int TOTAL = 8 * WB + NL;        // 8 warp buffers | interior 1/(lx+ly+lz) table
+};
+
+// out[i] = sum_l S_V[l][i] w[l] (TR: S^T w) or sum_l S_V[i][l] w[l]; coefficients are warp-uniform
+// kernel-parameter operands
+template <typename T, int K, int V, bool TR>
+__device__ __forceinline__ void sdot(const Coef2<T, K>& c, const T (&w)[2 * K - 1], T (&o)[2 * K - 1]) {
+  constexpr int NP = 2 * K - 1;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) o[i] = 0;
+#pragma unroll
+  for (int l = 0; l < NP; ++l)
+#pragma unroll
+    for (int i = 0; i < NP; ++i) o[i] = fma(TR ? c.S[V][l * NP + i] : c.S[V][i * NP + l], w[l], o[i]);
+}
+// same with the interior S held in registers (Sr[l * NP + i] = S_1[l][i])
+template <typename T, int K, bool TR, int M>
+__device__ __forceinline__ void sdot_reg(const T (&Sr)[M], const T (&w)[2 * K - 1], T (&o)[2 * K - 1]) {
+  constexpr int NP = 2 * K - 1;
+  static_assert(M == NP * NP, "register S");
+#pragma unroll
+  for (int i = 0; i < NP; ++i) o[i] = 0;
+#pragma unroll
+  for (int l = 0; l < NP; ++l)
+#pragma unroll
+    for (int i = 0; i < NP; ++i) o[i] = fma(TR ? Sr[l * NP + i] : Sr[i * NP + l], w[l], o[i]);
+}
+template <typename T, int K, bool TR>
+__device__ __forceinline__ void sdot_var(const Coef2<T, K>& c, int var, const T (&w)[2 * K - 1], T (&o)[2 * K - 1]) {
+  if (var == 1) sdot<T, K, 1, TR>(c, w, o);
+  else if (var == 0) sdot<T, K, 0, TR>(c, w, o);
+  else sdot<T, K, 2, TR>(c, w, o);
+}
+
+// x += omega h A~_v^{-1} R_v r, one warp per patch: lanes own patch lines; the six
+// contractions (S^T along x, y, z; scale by 1/(lam_x + lam_y + lam_z); S along z, y, x) run on
+// register lines with warp-uniform coefficients, the line transposes between axes go through a
+// per-warp shared-memory buffer (__syncwarp only).  The z stage does S_z^T, the scaling and S_z in
+// registers.  r lines are read from global memory, the x update is a read-modify-write (disjoint
+// patch list) or red.global.add (atomic AVS) restricted to the owned node planes.
+template <typename T, int K>
+__global__ void __launch_bounds__(256, 3) patch_fdm3d_kernel(const __grid_constant__ Fdm3P<T, K> P) {
+  using LY = Fdm3Layout<T, K>;
+  constexpr int NP = LY::NP, NL2 = LY::NL2, LPL = LY::LPL;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* const tab = reinterpret_cast<T*>(smem_raw) + 8 * LY::WB;    // interior variant 1/(lx + ly + lz)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T* const buf = reinterpret_cast<T*>(smem_raw) + warp * LY::WB;
+  for (int e = tid; e < LY::NL; e += 256) {
+    const int i = e % NP, j = (e / NP) % NP, m = e / NL2;
+    tab[e] = T(1) / (P.c.lam[1][i] + P.c.lam[1][j] + P.c.lam[1][m]);
+  }
+  __syncthreads();
+  const int64_t N = P.N, n = P.n;
+  const int Nm1 = int(N - 1);
+  // interior-variant S in registers for k <= 3 (every contraction of an interior patch then runs on
+  // register operands only)
+  constexpr bool REGS = K <= 3;
+  T Sr[REGS ? NP * NP : 1];
+#pragma unroll
+  for (int e = 0; e < (REGS ? NP * NP : 1); ++e) Sr[e] = P.c.S[1][e];
+  // uniform trip count over the CTA (the coefficient offsets below must be provably uniform)
+  const int64_t stride = int64_t(gridDim.x) * 8, first = int64_t(blockIdx.x) * 8;
+  const int iters = P.count > first ? int((P.count - first + stride - 1) / stride) : 0;
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+    const int64_t q = first + warp + int64_t(it) * stride;
+    if (q >= P.count) continue;
+    // divisions by the (runtime) box extents through multiply-high, corrected by at most one
+    auto udiv = [](unsigned a, unsigned d, unsigned m) {
+      unsigned qq = __umulhi(a, m);
+      if (a - qq * d >= d) ++qq;
+      return qq;
+    };
+    int vx, vy, vz;
+    if (P.list) {
+      const unsigned pid = unsigned(P.list[q]);
+      const unsigned t = udiv(pid, unsigned(Nm1), P.mag[0]), zz = udiv(pid, unsigned(Nm1 * Nm1), P.mag[1]);
+      vx = 1 + int(pid - t * unsigned(Nm1)); vy = 1 + int(t - zz * unsigned(Nm1)); vz = 1 + int(zz);
+    } else {
+      const unsigned iq = unsigned(q), rest = udiv(iq, unsigned(P.vcnt[0]), P.mag[0]);
+      const unsigned iz = udiv(rest, unsigned(P.vcnt[1]), P.mag[1]);
+      vx = P.vlo[0] + P.vstr * int(iq - rest * unsigned(P.vcnt[0]));
+      vy = P.vlo[1] + P.vstr * int(rest - iz * unsigned(P.vcnt[1]));
+      vz = P.vlo[2] + P.vstr * int(iz);
+    }
+    const int varx = variant_of(vx, N), vary = variant_of(vy, N), varz = variant_of(vz, N);
+    const int64_t g0 = ((int64_t(vz - 1) * K - P.row0) * n + int64_t(vy - 1) * K) * n + int64_t(vx - 1) * K;
+    const int64_t jz0 = int64_t(vz - 1) * K + 1;
+    const bool inner = (varx == 1 && vary == 1 && varz == 1);
+    auto patch = [&](auto INC) {
+      constexpr bool INNER = decltype(INC)::value;
+    T w[NP], o[NP], xl[NP];
+    // coefficients through an opaque zero offset per stage: loaded (LDCU) at the point of use as
+    // uniform operands instead of being hoisted into registers (one R2UR per DFMA otherwise)
+    // S_x^T on x lines (y, z) = (a, b), straight from global memory
+    const Coef2<T, K>& c0 = coef_at(P.c, (it * 8 + 0) * P.zero);
+#pragma unroll 1
+    for (int s = 0; s < LPL; ++s) {
+      const int ll = lane + 32 * s, la = ll % NP, lb = ll / NP;
+      if (ll >= NL2) continue;
+      const T* rp = P.r + g0 + (int64_t(lb) * n + la) * n;
+#pragma unroll
+      for (int l = 0; l < NP; ++l) w[l] = rp[l];
+      if (!P.atomic && LPL == 1) {      // the x line of the final stage is this lane's line: load it now
+        const T* xq = P.x + g0 + (int64_t(lb) * n + la) * n;
+#pragma unroll
+        for (int l = 0; l < NP; ++l) xl[l] = xq[l];
+      }
+      if constexpr (INNER && REGS) sdot_reg<T, K, true>(Sr, w, o); else sdot_var<T, K, true>(c0, varx, w, o);
+#pragma unroll
+      for (int i = 0; i < NP; ++i) buf[(lb * NP + la) * NP + i] = o[i];
+    }
+    __syncwarp();
+    // S_y^T on y lines (i, z) = (a, b)
+    const Coef2<T, K>& c1 = coef_at(P.c, (it * 8 + 1) * P.zero);
+#pragma unroll 1
+    for (int s = 0; s < LPL; ++s) {
+      const int ll = lane + 32 * s, la = ll % NP, lb = ll / NP;
+      if (ll >= NL2) continue;
+#pragma unroll
+      for (int l = 0; l < NP; ++l) w[l] = buf[(lb * NP + l) * NP + la];
+      if constexpr (INNER && REGS) sdot_reg<T, K, true>(Sr, w, o); else sdot_var<T, K, true>(c1, vary, w, o);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) buf[(lb * NP + j) * NP + la] = o[j];
+    }
+    __syncwarp();
+    // S_z^T, 1 / (lam_x + lam_y + lam_z), S_z on z lines (i, j) = (a, b)
+    const Coef2<T, K>& c2 = coef_at(P.c, (it * 8 + 2) * P.zero);
+#pragma unroll 1
+    for (int s = 0; s < LPL; ++s) {
+      const int ll = lane + 32 * s, la = ll % NP, lb = ll / NP;
+      if (ll >= NL2) continue;
+#pragma unroll
+      for (int l = 0; l < NP; ++l) w[l] = buf[(l * NP + lb) * NP + la];
+      if constexpr (INNER && REGS) sdot_reg<T, K, true>(Sr, w, o); else sdot_var<T, K, true>(c2, varz, w, o);
+      if (INNER) {
+#pragma unroll
+        for (int m = 0; m < NP; ++m) o[m] *= tab[(m * NP + lb) * NP + la];
+      } else {
+        const T lxy = P.c.lam[varx][la] + P.c.lam[vary][lb];
+#pragma unroll
+        for (int m = 0; m < NP; ++m) o[m] /= (lxy + P.c.lam[varz][m]);
+      }
+      if constexpr (INNER && REGS) sdot_reg<T, K, false>(Sr, o, w); else sdot_var<T, K, false>(c2, varz, o, w);
+#pragma unroll
+      for (int m = 0; m < NP; ++m) buf[(m * NP + lb) * NP + la] = w[m];
+    }
+    __syncwarp();
+    // S_y on y lines (i, z)
+    const Coef2<T, K>& c3 = coef_at(P.c, (it * 8 + 3) * P.zero);
+#pragma unroll 1
+    for (int s = 0; s < LPL; ++s) {
+      const int ll = lane + 32 * s, la = ll % NP, lb = ll / NP;
+      if (ll >= NL2) continue;
+#pragma unroll
+      for (int l = 0; l < NP; ++l) w[l] = buf[(lb * NP + l) * NP + la];
+      if constexpr (INNER && REGS) sdot_reg<T, K, false>(Sr, w, o); else sdot_var<T, K, false>(c3, vary, w, o);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) buf[(lb * NP + j) * NP + la] = o[j];
+    }
+    __syncwarp();
+    // S_x on x lines (y, z), x += omega h u on the owned planes
+    const Coef2<T, K>& c4 = coef_at(P.c, (it * 8 + 4) * P.zero);
+#pragma unroll 1
+    for (int s = 0; s < LPL; ++s) {
+      const int ll = lane + 32 * s, la = ll % NP, lb = ll / NP;
+      if (ll >= NL2) continue;
+#pragma unroll
+      for (int l = 0; l < NP; ++l) w[l] = buf[(lb * NP + la) * NP + l];
+      if constexpr (INNER && REGS) sdot_reg<T, K, false>(Sr, w, o); else sdot_var<T, K, false>(c4, varx, w, o);
+      const int64_t jz = jz0 + lb;
+      if (jz < P.out_lo || jz >= P.out_hi) continue;
+      T* xp = P.x + g0 + (int64_t(lb) * n + la) * n;
+      if (P.atomic) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) atomicAdd(xp + i, P.factor * o[i]);
+      } else if (LPL == 1) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) xp[i] = fma(P.factor, o[i], xl[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) xp[i] = fma(P.factor, o[i], xp[i]);
+      }
+    }
+    __syncwarp();
+    };
+    if (inner) patch(std::true_type{});
+    else patch(std::false_type{});
+  }
+}
+
 // ----------------------------------------------------------------------------- host side
 static SlabWindow full_window3(const FusedLevel& F) { return SlabWindow{0, F.n, 1, int64_t(F.k) * F.N}; }
 
@@ -440,6 +640,20 @@ struct PatchSet3 {
 };
 
 template <typename T, int K>
+static void launch_fdm3_cta(const Fdm3P<T, K>& p, int64_t count, cudaStream_t st) {
+  using LY = Fdm3CtaLayout<T, K>;
+  const size_t smem = sizeof(T) * size_t(LY::TOTAL);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(patch_fdm3d_cta_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(patch_fdm3d_cta_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    attr = true;
+  }
+  const int64_t grid = (count + LY::PB - 1) / LY::PB;
+  patch_fdm3d_cta_kernel<T, K><<<(unsigned)grid, 256, smem, st>>>(p);
+}
+
+template <typename T, int K>
 static void launch_fdm3(const FusedLevel& F, T omega, const T* r, T* x, const PatchSet3& ps, int atomic,
                         const SlabWindow& w, cudaStream_t st) {
   using LY = Fdm3Layout<T, K>;
@@ -455,11 +669,30 @@ static void launch_fdm3(const FusedLevel& F, T omega, const T* r, T* x, const Pa
   p.r = r; p.x = x; p.list = ps.list; p.count = ps.count; p.N = F.N; p.n = F.n;
   for (int a = 0; a < 3; ++a) { p.vlo[a] = ps.vlo[a]; p.vcnt[a] = ps.vcnt[a]; }
   p.vstr = ps.vstr;
+  {
+    const unsigned Nm1 = unsigned(F.N - 1);
+    const unsigned d0 = ps.list ? Nm1 : unsigned(std::max(1, ps.vcnt[0]));
+    const unsigned d1 = ps.list ? Nm1 * Nm1 : unsigned(std::max(1, ps.vcnt[1]));
+    p.mag[0] = unsigned(0xFFFFFFFFull / d0);
+    p.mag[1] = unsigned(0xFFFFFFFFull / d1);
+  }
   p.row0 = w.row0; p.lrows = w.lrows; p.out_lo = w.out_lo; p.out_hi = w.out_hi;
   p.factor = T(double(omega) * F.h);
   p.zero = 0;
   p.atomic = atomic;
-  const int64_t grid = (ps.count + LY::PB - 1) / LY::PB;
+  if (!atomic) {                 // disjoint list: CTA-cooperative kernel (measured faster)
+    launch_fdm3_cta<T, K>(p, ps.count, st);
+    return;
+  }
+  static int grid_cache = -1;
+  if (grid_cache < 0) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, patch_fdm3d_kernel<T, K>, 256, smem);
+    grid_cache = sms * std::max(per, 1);
+  }
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(grid_cache, (ps.count + 7) / 8));
   patch_fdm3d_kernel<T, K><<<(unsigned)grid, 256, smem, st>>>(p);
 }
 
