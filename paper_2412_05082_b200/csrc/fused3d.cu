@@ -79,16 +79,27 @@ __device__ __forceinline__ void load_planes_async(T* dst, const T* src, int64_t 
   const int64_t zlo = (row0 + 1 > 1) ? row0 + 1 : int64_t(1), zhi = (row0 + lrows < KN - 1) ? row0 + lrows : KN - 1;
   const bool inner = (X0 >= 1 && X0 + BW - 1 <= KN - 1 && Y0 >= 1 && Y0 + BW - 1 <= KN - 1 && z0 >= zlo &&
                       z0 + K - 1 <= zhi);
+  // one warp per (plane, box row), lanes along the row: the 64-bit row address once per row
   const T* base = src + ((z0 - 1 - row0) * n + (Y0 - 1)) * n + (X0 - 1);
-  for (int e = threadIdx.x; e < K * BW * BW; e += blockDim.x) {
-    const int pz = e / (BW * BW), rem = e - pz * (BW * BW), r = rem / BW, cc = rem - (rem / BW) * BW;
-    const int64_t off = ((int64_t)pz * n + r) * n + cc;
-    bool ok = inner;
-    if (!inner) {
-      const int64_t jz = z0 + pz, jy = Y0 + r, jx = X0 + cc;
-      ok = (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1 && jz >= zlo && jz <= zhi);
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool xin = (X0 >= 1 && X0 + BW - 1 <= KN - 1);
+  for (int pr = threadIdx.x >> 5; pr < K * BW; pr += nw) {
+    const int pz = pr / BW, r = pr - pz * BW;
+    const T* rowp = base + ((int64_t)pz * n + r) * n;
+    T* d = dst + (pz * BW + r) * PX;
+    const int64_t jz = z0 + pz, jy = Y0 + r;
+    const bool rok = inner || (jy >= 1 && jy <= KN - 1 && jz >= zlo && jz <= zhi);
+    if (inner || (rok && xin)) {
+#pragma unroll
+      for (int cc = lane; cc < BW; cc += 32) cp_async_elem(d + cc, rowp + cc, true);
+    } else {
+#pragma unroll
+      for (int cc = lane; cc < BW; cc += 32) {
+        const int64_t jx = X0 + cc;
+        const bool ok = rok && jx >= 1 && jx <= KN - 1;
+        cp_async_elem(d + cc, ok ? rowp + cc : src, ok);
+      }
     }
-    cp_async_elem(dst + (pz * BW + r) * PX + cc, ok ? base + off : src, ok);
   }
 }
 
@@ -134,8 +145,8 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
 #pragma unroll 1
     for (int it = 0; it < cdiv(K * BW * C, NT); ++it, ++round) {
       const int u = it * NT + tid;
-      if (u >= K * BW * C) continue;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      if (u >= K * BW * C) continue;
       const int r = u % BW, rest = u / BW, ci = rest % C, pz = rest / C;
       const int64_t cx = cx0 + ci;
       if (cx >= N) continue;
@@ -170,8 +181,8 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
 #pragma unroll 1
     for (int it = 0; it < cdiv(K * O * C, NT); ++it, ++round) {
       const int u = it * NT + tid;
-      if (u >= K * O * C) continue;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      if (u >= K * O * C) continue;
       const int col = u % O, rest = u / O, ci = rest % C, pz = rest / C;
       const int64_t cy = cy0 + ci;
       if (cy >= N) continue;
@@ -232,10 +243,10 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
     }
     // after this step the newest plane is (cz0 - 2 + s) K: layer cz = cz0 + s - 4 is complete
     const int64_t cz = cz0 + s - 4;
+    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
     if (s >= 4 && zown) {
       const int64_t jx = cx0 * K + ox, jy = cy0 * K + oy;
       if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1) {
-        const Coef2<T, K>& c = coef_at(P.c, (round++) * P.zero);
         const bool inner = (cz >= 2 && cz <= N - 2);
 #pragma unroll
         for (int p = 0; p < K; ++p) {

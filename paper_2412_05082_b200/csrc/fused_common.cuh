@@ -155,6 +155,27 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 template <typename T, int ROWS, int COLS, int PITCH>
 __device__ __forceinline__ void load_box_async(T* dst, const T* src, int64_t n, int64_t KN, int64_t Y0,
                                                int64_t X0, int64_t row0, int64_t lrows) {
+  const int64_t ylo = (row0 + 1 > 1) ? row0 + 1 : int64_t(1), yhi = (row0 + lrows < KN - 1) ? row0 + lrows : KN - 1;
+  const bool inner = (X0 >= 1 && X0 + COLS - 1 <= KN - 1 && Y0 >= ylo && Y0 + ROWS - 1 <= yhi);
+  const T* base = src + (Y0 - 1 - row0) * n + (X0 - 1);
+  if (inner) {
+    for (int e = threadIdx.x; e < ROWS * COLS; e += blockDim.x) {
+      const int r = e / COLS, c = e - (e / COLS) * COLS;
+      cp_async_elem(dst + r * PITCH + c, base + (int64_t)r * n + c, true);
+    }
+  } else {
+    for (int e = threadIdx.x; e < ROWS * COLS; e += blockDim.x) {
+      const int r = e / COLS, c = e - (e / COLS) * COLS;
+      const int64_t jy = Y0 + r, jx = X0 + c;
+      const bool ok = (jx >= 1 && jx <= KN - 1 && jy >= ylo && jy <= yhi);
+      cp_async_elem(dst + r * PITCH + c, ok ? base + (int64_t)r * n + c : src, ok);
+    }
+  }
+}
+
+template <typename T, int ROWS, int COLS, int PITCH>
+__device__ __forceinline__ void load_box_rows_async(T* dst, const T* src, int64_t n, int64_t KN, int64_t Y0,
+                                               int64_t X0, int64_t row0, int64_t lrows) {
   // one warp per box row, lanes along the row (no per-element index division)
   const int64_t ylo = (row0 + 1 > 1) ? row0 + 1 : int64_t(1), yhi = (row0 + lrows < KN - 1) ? row0 + lrows : KN - 1;
   const bool xin = (X0 >= 1 && X0 + COLS - 1 <= KN - 1);

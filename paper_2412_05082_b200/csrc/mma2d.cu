@@ -510,18 +510,35 @@ __global__ void __launch_bounds__(256, 4) patch_fdm2d_mma_kernel(const __grid_co
   const unsigned magic = unsigned(0xFFFFFFFFull / unsigned(Nm1));
   const int64_t n = P.n;
   const bool r0 = g < NP && 2 * q < NP, r1 = g < NP && 2 * q + 1 < NP;
-#pragma unroll 1
-  for (int64_t pi = int64_t(blockIdx.x) * (NT / 32) + warp; pi < P.count; pi += int64_t(gridDim.x) * (NT / 32)) {
+  // software pipeline: the next patch's coordinates and r fragment are loaded before this patch's
+  // DMMA chain runs (the r loads are the latency the warps otherwise wait on)
+  struct Item {
+    int varx, vary;
+    int64_t po;
+    double b0, b1;
+  };
+  auto fetch = [&](int64_t pi, Item& it) {
     const int pid = P.list ? P.list[pi] : int(pi);
     int qy = int(__umulhi(unsigned(pid), magic));        // pid / (N - 1), at most one short
     if (pid - qy * Nm1 >= Nm1) ++qy;
     const int vy = 1 + qy, vx = 1 + pid - qy * Nm1;
-    const int varx = vx == 1 ? 0 : (vx == Nm1 ? 2 : 1), vary = vy == 1 ? 0 : (vy == Nm1 ? 2 : 1);
-    const int64_t po = int64_t((vy - 1) * K + g) * n + (vx - 1) * K + 2 * q;   // node (jy0 + g, jx0 + 2q)
-    const double b0 = r0 ? __ldg(r + po) : 0.0, b1 = r1 ? __ldg(r + po + 1) : 0.0;
+    it.varx = vx == 1 ? 0 : (vx == Nm1 ? 2 : 1);
+    it.vary = vy == 1 ? 0 : (vy == Nm1 ? 2 : 1);
+    it.po = int64_t((vy - 1) * K + g) * n + (vx - 1) * K + 2 * q;   // node (jy0 + g, jx0 + 2q)
+    it.b0 = r0 ? __ldg(r + it.po) : 0.0;
+    it.b1 = r1 ? __ldg(r + it.po + 1) : 0.0;
+  };
+  const int64_t stride = int64_t(gridDim.x) * (NT / 32);
+  int64_t pi = int64_t(blockIdx.x) * (NT / 32) + warp;
+  Item cur;
+  if (pi < P.count) fetch(pi, cur);
+#pragma unroll 1
+  for (; pi < P.count; pi += stride) {
+    Item nxt;
+    if (pi + stride < P.count) fetch(pi + stride, nxt);
     double u0, u1;
-    patch_solve(ffs[varx][lane], ffs[vary][lane], sfs[varx * 3 + vary][lane], b0, b1, u0, u1);
-    double* xp = P.x + po;
+    patch_solve(ffs[cur.varx][lane], ffs[cur.vary][lane], sfs[cur.varx * 3 + cur.vary][lane], cur.b0, cur.b1, u0, u1);
+    double* xp = P.x + cur.po;
     if (atomic) {
       if (r0) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp), "d"(u0) : "memory");
       if (r1) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp + 1), "d"(u1) : "memory");
@@ -529,6 +546,7 @@ __global__ void __launch_bounds__(256, 4) patch_fdm2d_mma_kernel(const __grid_co
       if (r0) xp[0] += u0;
       if (r1) xp[1] += u1;
     }
+    cur = nxt;
   }
 }
 
