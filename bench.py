@@ -534,6 +534,29 @@ def main():
         res["mixed_speedup"] = round(res["fp64"]["seconds"] / res["mixed"]["seconds"], 3)
         line["pcg"] = res
         cp.close()
+        if (d == 2 and k == 4) or d == 3:
+            # cfg3 (BASELINE.json configs[2]): coloured multiplicative smoother, k = 4, N = 2048 (67.1M DoFs),
+            # one MVS step (omega = 1) with the symmetric colour order (Q11), FP32 vs FP64 cycle;
+            # 3D (cfg4, the paper's Fig. 4 setting): MVS omega = 0.7, N = 2^Lp
+            Lm = 11 if d == 2 else Lp
+            om_m = 1.0 if d == 2 else 0.7
+            cm = api.Context(d, k, Lm, device=local)
+            bm = cm.rhs(Lm)
+            rm = {}
+            for name, cdt in (("fp64", torch.float64), ("mixed", torch.float32)):
+                mg = api.MG("mvs", 1, om_m, symmetric=True, cycle_dtype=cdt)
+                cm.pcg(mg, bm, max_iter=2)
+                torch.cuda.synchronize()
+                xs, rep, hist = cm.pcg(mg, bm, max_iter=60)
+                rm[name] = {"seconds": round(rep["seconds"], 4), "iterations": rep["iterations"],
+                            "nu": round(rep["nu"], 2), "converged": rep["converged"]}
+            rm["dofs"] = cm.n_dofs(Lm)
+            rm["config"] = ((f"cfg3: 2D Q4, L=11 (N=2048), MVS 1+1 step omega=1 (8 colours" if d == 2 else
+                             f"cfg4: 3D Q{k}, L={Lm} (N={2 ** Lm}), MVS 1+1 step omega=0.7 (16 colours") +
+                            ", reversed order in post-smoothing), CG rtol 1e-8 (max 60 iterations), x0=0, paper load")
+            rm["mixed_speedup"] = round(rm["fp64"]["seconds"] / rm["mixed"]["seconds"], 3)
+            line["pcg_mvs"] = rm
+            cm.close()
     else:
         ctx.close()
 

@@ -427,3 +427,45 @@ def test_3d_chunked_stream_matches_oracle_rows(k, N):
         rb, ids = residual_on_box(k, 3, N, s, x, b, lo, hi)
         assert rel(r_f[ids], rb) <= FP64_TOL
     ctx.close()
+
+
+# ------------------------------------------------------------------------------ full bench sizes
+# BASELINE.json configs[1] / configs[3] at the sizes and in the launch configuration bench.py times
+# (atomic AVS step, fused kernels), checked on sampled outputs the oracle computes one by one
+# (local window assembly + dense surrogate solves; oracle.smoothers.avs_delta_sample).
+def _sample_ids(n, d, rng, m=48):
+    ids = set()
+    edge = [0, 1, n // 2, n - 2, n - 1]
+    for _ in range(m):
+        c = [int(rng.integers(0, n)) if rng.random() < 0.7 else int(rng.choice(edge)) for _ in range(d)]
+        ids.add(sum(c[a] * n ** a for a in range(d)))
+    return np.array(sorted(ids))
+
+
+@pytest.mark.parametrize("d,k,sm", [(2, 4, "avs_atomic"), (2, 4, "avs"), (2, 3, "avs_atomic"),
+                                    (3, 3, "avs_atomic"), (3, 2, "avs")])
+def test_full_size_sampled_avs(d, k, sm):
+    from c0ip_inputs import CFG2_CELLS, CFG4_CELLS
+    from oracle.smoothers import avs_delta_sample
+    from oracle.operator import residual_on_box
+    from paper_2412_05082_b200 import api
+    N = CFG2_CELLS[k] if d == 2 else CFG4_CELLS[k]
+    om = 0.25 if d == 2 else 0.1
+    ctx = api.Context(d, k, 3, cells_override=N)
+    x, b = random_xb(k, d, N)
+    n = k * N - 1
+    xt = torch.tensor(x, device=DEV)
+    bt = torch.tensor(b, device=DEV)
+    r = ctx.residual(3, bt, xt, torch.empty_like(xt)).cpu().numpy()
+    ctx.smooth(3, sm, 1, om, bt, xt)
+    dg = xt.cpu().numpy() - x
+    ctx.close()
+    rng = np.random.default_rng(7)
+    ids = _sample_ids(n, d, rng)
+    s = default_sigma(k)
+    do = avs_delta_sample(k, d, N, s, x, b, om, ids)
+    assert np.abs(dg[ids] - do).max() <= 1e-11 * np.abs(do).max(), np.abs(dg[ids] - do).max() / np.abs(do).max()
+    # residual rows at the same ids
+    ro = np.array([residual_on_box(k, d, N, s, x, b, [(g // n ** a) % n for a in range(d)],
+                                   [(g // n ** a) % n + 1 for a in range(d)])[0][0] for g in ids])
+    assert np.abs(r[ids] - ro).max() <= 1e-11 * np.abs(ro).max()
