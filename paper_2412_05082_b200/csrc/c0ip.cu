@@ -345,6 +345,10 @@ void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, b
             c0ip::fused_mvs_color<T>(*L.fused, L.colors_d.p + L.color_off[c], cnt, omega, b, x, st,
                                      &ctx->launches))
           continue;
+        if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
+            c0ip::fused3_mvs_color<T>(*L.fused, L.colors_d.p + L.color_off[c], cnt, omega, b, x, st,
+                                      &ctx->launches))
+          continue;
         apply_op<T>(ctx, L, x, b, t.sres.p, st);                 // residual per colour
         disjoint_patch_solve<T>(ctx, L, t.sres.p, x, omega, L.colors_d.p + L.color_off[c], cnt, st);
       }

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -618,6 +619,362 @@ __global__ void __launch_bounds__(256, 3) patch_fdm3d_kernel(const __grid_consta
   }
 }
 
+// ----------------------------------------------------------------------------- mvs3d
+// One colour of the coloured multiplicative smoother in 3D, fused per patch, one
+// warp per patch (k <= 3): the residual r_v = b - A x on the np^3 patch nodes is evaluated from x on
+// the patch footprint (patch cells plus their face neighbours; same-colour patches never
+// write it, so the in-place update is race-free) by sum factorisation of the six Kronecker terms of
+// Eq. c0iptensorvp3D, per axis with F = [(v-2)k, (v+2)k] (4k+1 nodes), W =
+// [(v-1)k, (v+1)k] (2k+1) and the patch nodes P ((v-1)k+1 .. (v+1)k-1, np):
+//   x stage (lanes <-> rows (y, z) of the cross F x W u W x F):  Xm = M^_x x on every cross row,
+//            Xb = B^_x x and Xl = L^_x x on the W x W rows (x in F, resp. W)
+//   y stage (lanes <-> lines (x, z)):  G1 = M^_y Xb + B^_y Xm + 2 L^_y Xl  (z in W)
+//                                      G2 = M^_y Xm                       (z in F)
+//                                      G3 = 2 M^_y Xl + 2 L^_y Xm          (z in W)
+//   z stage (lanes <-> lines (x, y)):  A x = M^_z G1 + B^_z G2 + L^_z G3 on P,  r = b - h^-1 A x
+// followed by the FDM solve on the same lines (S_z^T in registers, S_y^T, S_x^T / scale / S_x, S_y
+// through a per-warp buffer, S_z) and x += omega h u on the patch nodes.
+template <typename T, int K>
+struct Mvs3Layout {
+  static constexpr int NP = 2 * K - 1, W = 2 * K + 1, F = 4 * K + 1;
+  static constexpr int XM = F * F * NP;           // Xm[z][y][p] (full F x F index, cross rows filled)
+  static constexpr int XB = W * W * NP;           // Xb[z - K][y - K][p], Xl likewise
+  static constexpr int G1 = W * NP * NP, G2 = F * NP * NP, G3 = W * NP * NP;   // G[z][y'][x']
+  static constexpr int WARP = XM + 2 * XB + G1 + G2 + G3;                   // per warp (FDM buffer aliases Xm)
+  static constexpr int NW = 4;                    // warps per CTA
+  // coefficient tables per axis variant v: Bt[v][p][f] (P x F), Mt[v][p][w], Lt[v][p][w] (P x W),
+  // S[v][l][i], lam[v][i]
+  static constexpr int TAB = 3 * (NP * F + 2 * NP * W + NP * NP + NP);
+  static constexpr int TOTAL = NW * WARP + TAB;
+};
+
+template <typename T, int K>
+__global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP<T, K> P) {
+  using LY = Mvs3Layout<T, K>;
+  constexpr int NP = LY::NP, W = LY::W, F = LY::F, NW = LY::NW;
+  constexpr int TB = NP * F, TM = NP * W, TS = NP * NP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* const tabs = reinterpret_cast<T*>(smem_raw) + NW * LY::WARP;
+  T* const Bt = tabs;                         // [3][NP][F]
+  T* const Mt = Bt + 3 * TB;                  // [3][NP][W]
+  T* const Lt = Mt + 3 * TM;                  // [3][NP][W]
+  T* const St = Lt + 3 * TM;                  // [3][NP][NP]  S[l][i]
+  T* const Lam = St + 3 * TS;                 // [3][NP]
+  const int64_t N = P.N, n = P.n, KN = K * N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // tables of the three axis variants (representative vertices 1, N/2, N-1; see mvs2d_mma)
+  for (int e = tid; e < 3 * (TB + 2 * TM); e += blockDim.x) {
+    int v, p, c, which;
+    if (e < 3 * TB) { v = e / TB; p = (e % TB) / F; c = e % F; which = 0; }
+    else if (e < 3 * (TB + TM)) { const int r = e - 3 * TB; v = r / TM; p = (r % TM) / W; c = r % W; which = 1; }
+    else { const int r = e - 3 * (TB + TM); v = r / TM; p = (r % TM) / W; c = r % W; which = 2; }
+    const int64_t vr = v == 0 ? 1 : (v == 1 ? N / 2 : N - 1);
+    const int64_t jo = (vr - 1) * K + 1 + p;
+    const int64_t ji = which == 0 ? (vr - 2) * K + c : (vr - 1) * K + c;
+    // op1d of mma2d.cu, inlined: full-band 1D coefficient
+    T val = 0;
+    const int64_t off = ji - jo;
+    if (ji >= 1 && ji <= KN - 1) {
+      const int sp = special_row<K>(jo, N);
+      if (which == 0) {
+        if (off >= -2 * K && off <= 2 * K) val = sp >= 0 ? P.c.BS[sp][off + 2 * K] : P.c.BI[jo % K][off + 2 * K];
+      } else if (sp >= 0) {
+        if (off >= -2 * K && off <= 2 * K) val = which == 1 ? P.c.MS[sp][off + 2 * K] : P.c.LS[sp][off + 2 * K];
+      } else if (off >= -K && off <= K) {
+        val = which == 1 ? P.c.MI[jo % K][off + K] : P.c.LI[jo % K][off + K];
+      }
+    }
+    tabs[e] = val;
+  }
+  for (int e = tid; e < 3 * TS; e += blockDim.x) St[e] = P.c.S[e / TS][e % TS];
+  for (int e = tid; e < 3 * NP; e += blockDim.x) Lam[e] = P.c.lam[e / NP][e % NP];
+  __syncthreads();
+
+  T* const xm = reinterpret_cast<T*>(smem_raw) + warp * LY::WARP;
+  T* const xb = xm + LY::XM;
+  T* const xl = xb + LY::XB;
+  T* const g1 = xl + LY::XB;
+  T* const g2 = g1 + LY::G1;
+  T* const g3 = g2 + LY::G2;
+  T* const buf = xm;                          // FDM transposes (np^3), Xm is dead by then
+  const int Nm1 = int(N - 1);
+  const T* __restrict__ X = P.x;
+
+#pragma unroll 1
+  for (int64_t pi = int64_t(blockIdx.x) * NW + warp; pi < P.count; pi += int64_t(gridDim.x) * NW) {
+    const int pid = P.list[pi];
+    const int vx = 1 + pid % Nm1, vy = 1 + (pid / Nm1) % Nm1, vz = 1 + pid / (Nm1 * Nm1);
+    const int varx = variant_of(vx, N), vary = variant_of(vy, N), varz = variant_of(vz, N);
+    const int64_t jx0 = int64_t(vx - 2) * K, jy0 = int64_t(vy - 2) * K, jz0 = int64_t(vz - 2) * K;   // F origin
+    const bool inner = jx0 >= 1 && jx0 + F - 1 <= KN - 1 && jy0 >= 1 && jy0 + F - 1 <= KN - 1 && jz0 >= 1 &&
+                       jz0 + F - 1 <= KN - 1;
+    auto ldx = [&](int z, int y, int xx) -> T {            // x at F-local (xx, y, z)
+      const int64_t gz = jz0 + z, gy = jy0 + y, gx = jx0 + xx;
+      if (!inner && (gx < 1 || gx > KN - 1 || gy < 1 || gy > KN - 1 || gz < 1 || gz > KN - 1)) return T(0);
+      return __ldg(X + ((gz - 1) * n + (gy - 1)) * n + (gx - 1));
+    };
+    const T* bx = Bt + varx * TB;
+    const T* mx = Mt + varx * TM;
+    const T* lx = Lt + varx * TM;
+    // ---- x stage: W x W rows (Xm, Xb, Xl)
+#pragma unroll 1
+    for (int r = lane; r < W * W; r += 32) {
+      const int y = K + r % W, z = K + r / W;
+      T w[F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) w[f] = ldx(z, y, f);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        T ab = 0, am = 0, al = 0;
+#pragma unroll
+        for (int f = 0; f < F; ++f) ab = fma(bx[p * F + f], w[f], ab);
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+          am = fma(mx[p * W + c], w[K + c], am);
+          al = fma(lx[p * W + c], w[K + c], al);
+        }
+        xm[(z * F + y) * NP + p] = am;
+        xb[((z - K) * W + (y - K)) * NP + p] = ab;
+        xl[((z - K) * W + (y - K)) * NP + p] = al;
+      }
+    }
+    // ---- x stage: the other cross rows (y in F \ W, z in W) and (y in W, z in F \ W): Xm only
+#pragma unroll 1
+    for (int r = lane; r < 4 * K * W; r += 32) {
+      int y, z;
+      const int h = r / (2 * K * W), rr = r % (2 * K * W), o = rr % (2 * K), t = rr / (2 * K);
+      const int fo = o < K ? o : o + W;             // F \ W index
+      if (h == 0) { y = fo; z = K + t; } else { y = K + t; z = fo; }
+      T w[W];
+#pragma unroll
+      for (int c = 0; c < W; ++c) w[c] = ldx(z, y, K + c);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        T am = 0;
+#pragma unroll
+        for (int c = 0; c < W; ++c) am = fma(mx[p * W + c], w[c], am);
+        xm[(z * F + y) * NP + p] = am;
+      }
+    }
+    __syncwarp();
+    // ---- y stage
+    const T* by = Bt + vary * TB;
+    const T* my = Mt + vary * TM;
+    const T* ly = Lt + vary * TM;
+#pragma unroll 1
+    for (int l = lane; l < (2 * W + F) * NP; l += 32) {
+      const int xq = l % NP, zl = l / NP;
+      if (zl < W) {                                   // G1 on z = K + zl
+        const int z = K + zl;
+        T wb[W], wl[W], wm[F];
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+          wb[c] = xb[(zl * W + c) * NP + xq];
+          wl[c] = xl[(zl * W + c) * NP + xq];
+        }
+#pragma unroll
+        for (int f = 0; f < F; ++f) wm[f] = xm[(z * F + f) * NP + xq];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          T a = 0;
+#pragma unroll
+          for (int c = 0; c < W; ++c) a = fma(my[p * W + c], wb[c], fma(T(2) * ly[p * W + c], wl[c], a));
+#pragma unroll
+          for (int f = 0; f < F; ++f) a = fma(by[p * F + f], wm[f], a);
+          g1[(zl * NP + p) * NP + xq] = a;
+        }
+      } else if (zl < 2 * W) {                        // G3 on z = K + (zl - W)
+        const int z3 = zl - W, z = K + z3;
+        T wl[W], wm[W];
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+          wl[c] = xl[(z3 * W + c) * NP + xq];
+          wm[c] = xm[(z * F + K + c) * NP + xq];
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          T a = 0;
+#pragma unroll
+          for (int c = 0; c < W; ++c) a = fma(my[p * W + c], wl[c], fma(ly[p * W + c], wm[c], a));
+          g3[(z3 * NP + p) * NP + xq] = T(2) * a;
+        }
+      } else {                                        // G2 on z = zl - 2W in F
+        const int z = zl - 2 * W;
+        T wm[W];
+#pragma unroll
+        for (int c = 0; c < W; ++c) wm[c] = xm[(z * F + K + c) * NP + xq];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          T a = 0;
+#pragma unroll
+          for (int c = 0; c < W; ++c) a = fma(my[p * W + c], wm[c], a);
+          g2[(z * NP + p) * NP + xq] = a;
+        }
+      }
+    }
+    __syncwarp();
+    // ---- z stage + residual + S_z^T (lanes <-> (x', y') lines)
+    const T* bz = Bt + varz * TB;
+    const T* mz = Mt + varz * TM;
+    const T* lz = Lt + varz * TM;
+    const T* sx = St + varx * TS;
+    const T* sy = St + vary * TS;
+    const T* sz = St + varz * TS;
+    const bool act = lane < NP * NP;
+    const int xq = lane % NP, yq = lane / NP;
+    const int64_t gx = jx0 + K + 1 + xq, gy = jy0 + K + 1 + yq;     // patch node (global node index)
+    T rz[NP];
+    if (act) {
+      T w1[W], w2[F], w3[W];
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        w1[c] = g1[(c * NP + yq) * NP + xq];
+        w3[c] = g3[(c * NP + yq) * NP + xq];
+      }
+#pragma unroll
+      for (int f = 0; f < F; ++f) w2[f] = g2[(f * NP + yq) * NP + xq];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        T a = 0;
+#pragma unroll
+        for (int c = 0; c < W; ++c) a = fma(mz[p * W + c], w1[c], fma(lz[p * W + c], w3[c], a));
+#pragma unroll
+        for (int f = 0; f < F; ++f) a = fma(bz[p * F + f], w2[f], a);
+        const int64_t gz = jz0 + K + 1 + p;
+        rz[p] = fma(-P.scale, a, P.b[((gz - 1) * n + (gy - 1)) * n + (gx - 1)]);
+      }
+      // S_z^T on the z line
+      T o[NP];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) o[i] = 0;
+#pragma unroll
+      for (int l = 0; l < NP; ++l)
+#pragma unroll
+        for (int i = 0; i < NP; ++i) o[i] = fma(sz[l * NP + i], rz[l], o[i]);
+#pragma unroll
+      for (int i = 0; i < NP; ++i) buf[(i * NP + yq) * NP + xq] = o[i];    // buf[z'][y][x]
+    }
+    __syncwarp();
+    // S_y^T on y lines (x, z')
+    if (act) {
+      const int xa = lane % NP, zb = lane / NP;
+      T w[NP], o[NP];
+#pragma unroll
+      for (int l = 0; l < NP; ++l) w[l] = buf[(zb * NP + l) * NP + xa];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) o[i] = 0;
+#pragma unroll
+      for (int l = 0; l < NP; ++l)
+#pragma unroll
+        for (int i = 0; i < NP; ++i) o[i] = fma(sy[l * NP + i], w[l], o[i]);
+#pragma unroll
+      for (int i = 0; i < NP; ++i) buf[(zb * NP + i) * NP + xa] = o[i];
+    }
+    __syncwarp();
+    // S_x^T, scale by omega h / (lam_x + lam_y + lam_z), S_x on x lines (y', z')
+    if (act) {
+      const int ya = lane % NP, zb = lane / NP;
+      T w[NP], o[NP];
+#pragma unroll
+      for (int l = 0; l < NP; ++l) w[l] = buf[(zb * NP + ya) * NP + l];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) o[i] = 0;
+#pragma unroll
+      for (int l = 0; l < NP; ++l)
+#pragma unroll
+        for (int i = 0; i < NP; ++i) o[i] = fma(sx[l * NP + i], w[l], o[i]);
+      const T lyz = Lam[vary * NP + ya] + Lam[varz * NP + zb];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) o[i] = P.factor * o[i] / (Lam[varx * NP + i] + lyz);
+#pragma unroll
+      for (int l = 0; l < NP; ++l) w[l] = 0;
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int l = 0; l < NP; ++l) w[l] = fma(sx[l * NP + i], o[i], w[l]);
+#pragma unroll
+      for (int l = 0; l < NP; ++l) buf[(zb * NP + ya) * NP + l] = w[l];
+    }
+    __syncwarp();
+    // S_y on y lines (x, z')
+    if (act) {
+      const int xa = lane % NP, zb = lane / NP;
+      T w[NP], o[NP];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) w[i] = buf[(zb * NP + i) * NP + xa];
+#pragma unroll
+      for (int l = 0; l < NP; ++l) o[l] = 0;
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int l = 0; l < NP; ++l) o[l] = fma(sy[l * NP + i], w[i], o[l]);
+#pragma unroll
+      for (int l = 0; l < NP; ++l) buf[(zb * NP + l) * NP + xa] = o[l];
+    }
+    __syncwarp();
+    // S_z on z lines (x, y), x += u on the patch nodes (disjoint within the colour)
+    if (act) {
+      T w[NP], o[NP];
+#pragma unroll
+      for (int i = 0; i < NP; ++i) w[i] = buf[(i * NP + yq) * NP + xq];
+#pragma unroll
+      for (int l = 0; l < NP; ++l) o[l] = 0;
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+#pragma unroll
+        for (int l = 0; l < NP; ++l) o[l] = fma(sz[l * NP + i], w[i], o[l]);
+#pragma unroll
+      for (int l = 0; l < NP; ++l) {
+        const int64_t gz = jz0 + K + 1 + l;
+        T* xp = P.x + ((gz - 1) * n + (gy - 1)) * n + (gx - 1);
+        *xp += o[l];
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <typename T, int K>
+static void launch_mvs3(const FusedLevel& F, const int32_t* list, int64_t count, T omega, const T* b, T* x,
+                        cudaStream_t st) {
+  using LY = Mvs3Layout<T, K>;
+  const size_t smem = sizeof(T) * size_t(LY::TOTAL);
+  static int grid_cache = -1;
+  if (grid_cache < 0) {
+    cudaFuncSetAttribute(mvs3d_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(mvs3d_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mvs3d_kernel<T, K>, 128, smem);
+    grid_cache = sms * std::max(per, 1);
+  }
+  MvsP<T, K> p;
+  std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
+  p.x = x; p.b = b; p.list = list; p.count = count; p.N = F.N; p.n = F.n;
+  p.scale = T(1.0 / F.h);                  // 3D: A = h^-1 A^
+  p.factor = T(double(omega) * F.h);       //     A~^-1 = h A^~^-1
+  p.zero = 0;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid_cache, (count + LY::NW - 1) / LY::NW));
+  mvs3d_kernel<T, K><<<grid, 128, smem, st>>>(p);
+}
+
+template <typename T>
+bool fused3_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega, const T* b, T* x, cudaStream_t st,
+                      int64_t* launches) {
+  if (F.d != 3 || count == 0) return count == 0 && F.d == 3;
+  if (std::getenv("C0IP_NO_MVS3")) return false;
+  switch (F.k) {
+    case 2: launch_mvs3<T, 2>(F, list, count, omega, b, x, st); break;
+    case 3: launch_mvs3<T, 3>(F, list, count, omega, b, x, st); break;
+    default: return false;
+  }
+  (*launches)++;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("fused mvs3d launch: ") + cudaGetErrorString(e));
+  return true;
+}
+
 // ----------------------------------------------------------------------------- host side
 static SlabWindow full_window3(const FusedLevel& F) { return SlabWindow{0, F.n, 1, int64_t(F.k) * F.N}; }
 
@@ -799,6 +1156,10 @@ bool fused3_fdm_window(FusedLevel& F, T omega, const T* r, T* x, bool atomic, cu
   return true;
 }
 
+template bool fused3_mvs_color<double>(FusedLevel&, const int32_t*, int64_t, double, const double*, double*,
+                                       cudaStream_t, int64_t*);
+template bool fused3_mvs_color<float>(FusedLevel&, const int32_t*, int64_t, float, const float*, float*, cudaStream_t,
+                                      int64_t*);
 template bool fused3_apply<double>(FusedLevel&, const double*, const double*, double*, cudaStream_t, int64_t*,
                                    const SlabWindow*);
 template bool fused3_apply<float>(FusedLevel&, const float*, const float*, float*, cudaStream_t, int64_t*,

@@ -56,6 +56,10 @@ template <typename T>
 bool fused3_fdm_window(FusedLevel& F, T omega, const T* r, T* x, bool atomic, cudaStream_t st, int64_t* launches,
                        const SlabWindow* win = nullptr);
 int fused_dim(const FusedLevel& F);
+// one colour of the 3D coloured MVS fused per patch (residual on the footprint + FDM + update), k <= 3
+template <typename T>
+bool fused3_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega, const T* b, T* x,
+                      cudaStream_t st, int64_t* launches);
 
 // FP64 tensor-core (DMMA) kernels (mma2d.cu); false if the level / degree is not covered
 // (2D, k = 3, 4) or C0IP_NO_MMA is set
