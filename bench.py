@@ -508,7 +508,8 @@ def main():
         "matvec": {"value": round(ndofs * world / (t_mv_ms * 1e-3) / 1e9, 3), "unit": "GDoF/s",
                    "ms": round(t_mv_ms, 4)},
         "mvs": {"value": round(ndofs * world / (t_mvs_ms * 1e-3) / 1e9, 3), "unit": "GDoF/s",
-                "ms": round(t_mvs_ms, 4), "note": "one coloured MVS step, 8 colours, omega=1"},
+                "ms": round(t_mvs_ms, 4),
+                "note": f"one coloured MVS step, {2 ** (d + 1)} colours, omega={om_m}"},
         "avs_deterministic": {"value": round(ndofs * world / (t_atomic_ms * 1e-3) / 1e9, 3), "unit": "GDoF/s",
                               "ms": round(t_atomic_ms, 4)},
         "residual_ms": round(t_res_ms, 4), "fdm_ms": round(t_fdm_ms, 4),

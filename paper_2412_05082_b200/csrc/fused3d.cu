@@ -716,44 +716,87 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
     const T* bx = Bt + varx * TB;
     const T* mx = Mt + varx * TM;
     const T* lx = Lt + varx * TM;
-    // ---- x stage: W x W rows (Xm, Xb, Xl)
-#pragma unroll 1
-    for (int r = lane; r < W * W; r += 32) {
-      const int y = K + r % W, z = K + r / W;
-      T w[F];
+    // ---- x stage: W x W rows (Xm, Xb, Xl); RB1 rows per lane share every coefficient load
+    {
+      constexpr int RB1 = cdiv(W * W, 32), L1 = cdiv(W * W, RB1);
+      if (lane < L1) {
+        T w[RB1][F];
+        int ry[RB1], rzz[RB1];
+        bool ok[RB1];
 #pragma unroll
-      for (int f = 0; f < F; ++f) w[f] = ldx(z, y, f);
+        for (int j = 0; j < RB1; ++j) {
+          const int r = lane + j * L1;
+          ok[j] = r < W * W;
+          const int rc = ok[j] ? r : 0;
+          ry[j] = K + rc % W;
+          rzz[j] = K + rc / W;
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        T ab = 0, am = 0, al = 0;
-#pragma unroll
-        for (int f = 0; f < F; ++f) ab = fma(bx[p * F + f], w[f], ab);
-#pragma unroll
-        for (int c = 0; c < W; ++c) {
-          am = fma(mx[p * W + c], w[K + c], am);
-          al = fma(lx[p * W + c], w[K + c], al);
+          for (int f = 0; f < F; ++f) w[j][f] = ldx(rzz[j], ry[j], f);
         }
-        xm[(z * F + y) * NP + p] = am;
-        xb[((z - K) * W + (y - K)) * NP + p] = ab;
-        xl[((z - K) * W + (y - K)) * NP + p] = al;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          T ab[RB1], am[RB1], al[RB1];
+#pragma unroll
+          for (int j = 0; j < RB1; ++j) ab[j] = am[j] = al[j] = 0;
+#pragma unroll
+          for (int f = 0; f < F; ++f) {
+            const T cb = bx[p * F + f];
+#pragma unroll
+            for (int j = 0; j < RB1; ++j) ab[j] = fma(cb, w[j][f], ab[j]);
+          }
+#pragma unroll
+          for (int c = 0; c < W; ++c) {
+            const T cm = mx[p * W + c], cl = lx[p * W + c];
+#pragma unroll
+            for (int j = 0; j < RB1; ++j) {
+              am[j] = fma(cm, w[j][K + c], am[j]);
+              al[j] = fma(cl, w[j][K + c], al[j]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < RB1; ++j) {
+            if (!ok[j]) continue;
+            const int y = ry[j], z = rzz[j];
+            xm[(z * F + y) * NP + p] = am[j];
+            xb[((z - K) * W + (y - K)) * NP + p] = ab[j];
+            xl[((z - K) * W + (y - K)) * NP + p] = al[j];
+          }
+        }
       }
     }
     // ---- x stage: the other cross rows (y in F \ W, z in W) and (y in W, z in F \ W): Xm only
-#pragma unroll 1
-    for (int r = lane; r < 4 * K * W; r += 32) {
-      int y, z;
-      const int h = r / (2 * K * W), rr = r % (2 * K * W), o = rr % (2 * K), t = rr / (2 * K);
-      const int fo = o < K ? o : o + W;             // F \ W index
-      if (h == 0) { y = fo; z = K + t; } else { y = K + t; z = fo; }
-      T w[W];
+    {
+      constexpr int NR2 = 4 * K * W, RB2 = cdiv(NR2, 32), L2 = cdiv(NR2, RB2);
+      if (lane < L2) {
+        T w[RB2][W];
+        int ry[RB2], rzz[RB2];
+        bool ok[RB2];
 #pragma unroll
-      for (int c = 0; c < W; ++c) w[c] = ldx(z, y, K + c);
+        for (int j = 0; j < RB2; ++j) {
+          const int r0 = lane + j * L2;
+          ok[j] = r0 < NR2;
+          const int r = ok[j] ? r0 : 0;
+          const int h = r / (2 * K * W), rr = r % (2 * K * W), o = rr % (2 * K), t = rr / (2 * K);
+          const int fo = o < K ? o : o + W;             // F \ W index
+          if (h == 0) { ry[j] = fo; rzz[j] = K + t; } else { ry[j] = K + t; rzz[j] = fo; }
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        T am = 0;
+          for (int c = 0; c < W; ++c) w[j][c] = ldx(rzz[j], ry[j], K + c);
+        }
 #pragma unroll
-        for (int c = 0; c < W; ++c) am = fma(mx[p * W + c], w[c], am);
-        xm[(z * F + y) * NP + p] = am;
+        for (int p = 0; p < NP; ++p) {
+          T am[RB2];
+#pragma unroll
+          for (int j = 0; j < RB2; ++j) am[j] = 0;
+#pragma unroll
+          for (int c = 0; c < W; ++c) {
+            const T cm = mx[p * W + c];
+#pragma unroll
+            for (int j = 0; j < RB2; ++j) am[j] = fma(cm, w[j][c], am[j]);
+          }
+#pragma unroll
+          for (int j = 0; j < RB2; ++j)
+            if (ok[j]) xm[(rzz[j] * F + ry[j]) * NP + p] = am[j];
+        }
       }
     }
     __syncwarp();
