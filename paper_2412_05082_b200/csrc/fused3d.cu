@@ -21,6 +21,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "fused_common.cuh"
 
@@ -634,6 +635,24 @@ __global__ void __launch_bounds__(256, 3) patch_fdm3d_kernel(const __grid_consta
 //   z stage (lanes <-> lines (x, y)):  A x = M^_z G1 + B^_z G2 + L^_z G3 on P,  r = b - h^-1 A x
 // followed by the FDM solve on the same lines (S_z^T in registers, S_y^T, S_x^T / scale / S_x, S_y
 // through a per-warp buffer, S_z) and x += omega h u on the patch nodes.
+// acc[j] += c * w[j] for RB lines sharing the coefficient c; FP32 pairs go through the packed
+// FFMA2 (f32x2 FMA with a scalar operand, sm_100a): two FMAs per issue slot
+template <typename T, int RB>
+__device__ __forceinline__ void fma_lines(T c, const T (&w)[RB], T (&acc)[RB]) {
+  if constexpr (std::is_same<T, float>::value) {
+#pragma unroll
+    for (int j = 0; j + 1 < RB; j += 2) {
+      const float2 r = __ffma2_rn(make_float2(c, c), make_float2(w[j], w[j + 1]), make_float2(acc[j], acc[j + 1]));
+      acc[j] = r.x;
+      acc[j + 1] = r.y;
+    }
+    if constexpr (RB % 2 == 1) acc[RB - 1] = fmaf(c, w[RB - 1], acc[RB - 1]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < RB; ++j) acc[j] = fma(c, w[j], acc[j]);
+  }
+}
+
 template <typename T, int K>
 struct Mvs3Layout {
   static constexpr int NP = 2 * K - 1, W = 2 * K + 1, F = 4 * K + 1;
@@ -720,7 +739,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
     {
       constexpr int RB1 = cdiv(W * W, 32), L1 = cdiv(W * W, RB1);
       if (lane < L1) {
-        T w[RB1][F];
+        T w[F][RB1];
         int ry[RB1], rzz[RB1];
         bool ok[RB1];
 #pragma unroll
@@ -731,7 +750,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
           ry[j] = K + rc % W;
           rzz[j] = K + rc / W;
 #pragma unroll
-          for (int f = 0; f < F; ++f) w[j][f] = ldx(rzz[j], ry[j], f);
+          for (int f = 0; f < F; ++f) w[f][j] = ldx(rzz[j], ry[j], f);
         }
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -739,19 +758,11 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
 #pragma unroll
           for (int j = 0; j < RB1; ++j) ab[j] = am[j] = al[j] = 0;
 #pragma unroll
-          for (int f = 0; f < F; ++f) {
-            const T cb = bx[p * F + f];
-#pragma unroll
-            for (int j = 0; j < RB1; ++j) ab[j] = fma(cb, w[j][f], ab[j]);
-          }
+          for (int f = 0; f < F; ++f) fma_lines<T, RB1>(bx[p * F + f], w[f], ab);
 #pragma unroll
           for (int c = 0; c < W; ++c) {
-            const T cm = mx[p * W + c], cl = lx[p * W + c];
-#pragma unroll
-            for (int j = 0; j < RB1; ++j) {
-              am[j] = fma(cm, w[j][K + c], am[j]);
-              al[j] = fma(cl, w[j][K + c], al[j]);
-            }
+            fma_lines<T, RB1>(mx[p * W + c], w[K + c], am);
+            fma_lines<T, RB1>(lx[p * W + c], w[K + c], al);
           }
 #pragma unroll
           for (int j = 0; j < RB1; ++j) {
@@ -768,7 +779,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
     {
       constexpr int NR2 = 4 * K * W, RB2 = cdiv(NR2, 32), L2 = cdiv(NR2, RB2);
       if (lane < L2) {
-        T w[RB2][W];
+        T w[W][RB2];
         int ry[RB2], rzz[RB2];
         bool ok[RB2];
 #pragma unroll
@@ -780,7 +791,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
           const int fo = o < K ? o : o + W;             // F \ W index
           if (h == 0) { ry[j] = fo; rzz[j] = K + t; } else { ry[j] = K + t; rzz[j] = fo; }
 #pragma unroll
-          for (int c = 0; c < W; ++c) w[j][c] = ldx(rzz[j], ry[j], K + c);
+          for (int c = 0; c < W; ++c) w[c][j] = ldx(rzz[j], ry[j], K + c);
         }
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -788,11 +799,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
 #pragma unroll
           for (int j = 0; j < RB2; ++j) am[j] = 0;
 #pragma unroll
-          for (int c = 0; c < W; ++c) {
-            const T cm = mx[p * W + c];
-#pragma unroll
-            for (int j = 0; j < RB2; ++j) am[j] = fma(cm, w[j][c], am[j]);
-          }
+          for (int c = 0; c < W; ++c) fma_lines<T, RB2>(mx[p * W + c], w[c], am);
 #pragma unroll
           for (int j = 0; j < RB2; ++j)
             if (ok[j]) xm[(rzz[j] * F + ry[j]) * NP + p] = am[j];

@@ -392,18 +392,32 @@ def test_apply_residual_3d_fused(d, k, N):
     assert rel(y32, A @ xi) <= FP32_TOL
 
 
-@pytest.mark.parametrize("sm", ["avs", "avs_colored", "mvs"])
+@pytest.mark.parametrize("sm", ["avs", "avs_colored", "avs_atomic", "mvs", "mvs_rev"])
 @pytest.mark.parametrize("d,k,N", CASES_3D_FUSED[:3])
 def test_smoothers_3d_fused(d, k, N, sm):
     ctx, L = ctx_for(d, k, N)
     ctx.set_path(False)
     A, ps = oracle(d, k, N)
     x, b = random_xb(k, d, N)
-    om = 0.7 if sm == "mvs" else 0.1
+    rev = sm == "mvs_rev"
+    smc = "mvs" if rev else sm
+    om = 0.7 if smc == "mvs" else 0.1
+
+    def ref(xi, bi):
+        return mvs_step(A, ps, xi, bi, om, reverse=rev) if smc == "mvs" else avs_step(A, ps, xi, bi, om)
     xt = torch.tensor(x, device=DEV)
-    ctx.smooth(L, sm, 1, om, torch.tensor(b, device=DEV), xt)
-    do = (mvs_step(A, ps, x, b, om) if sm == "mvs" else avs_step(A, ps, x, b, om)) - x
+    ctx.smooth(L, smc, 1, om, torch.tensor(b, device=DEV), xt, reverse=rev)
+    do = ref(x, b) - x
     assert rel(xt.cpu().numpy() - x, do) <= FP64_TOL
+    # FP32 (the mixed-precision cycle's kernels) on the RN-rounded inputs
+    xi, bi = x.astype(np.float32).astype(np.float64), b.astype(np.float32).astype(np.float64)
+    x32 = torch.tensor(xi, device=DEV, dtype=torch.float32)
+    ctx.smooth(L, smc, 1, om, torch.tensor(bi, device=DEV, dtype=torch.float32), x32, reverse=rev)
+    xo32 = ref(xi, bi)
+    xg32 = x32.cpu().numpy().astype(np.float64)
+    dtol = fp32_delta_tol(ps)
+    assert rel(xg32 - xi, xo32 - xi) <= dtol
+    assert rel(xg32, xo32) <= max(FP32_TOL, dtol * np.linalg.norm(xo32 - xi) / np.linalg.norm(xo32))
 
 
 @pytest.mark.parametrize("k,N", [(2, 40), (3, 36)])
