@@ -510,6 +510,47 @@ __global__ void __launch_bounds__(256, 4) patch_fdm2d_mma_kernel(const __grid_co
   const unsigned magic = unsigned(0xFFFFFFFFull / unsigned(Nm1));
   const int64_t n = P.n;
   const bool r0 = g < NP && 2 * q < NP, r1 = g < NP && 2 * q + 1 < NP;
+  if (!P.list && atomic) {
+    // every patch (atomic AVS): warp tasks are runs of RUN consecutive patches along x of one patch
+    // row, so the patch origin advances by K nodes per patch (no index division), the interior
+    // patches use the register fragments, and the next patch's r fragment is loaded while the current
+    // chain runs
+    constexpr int RUN = 32;
+    const int nrun = (Nm1 + RUN - 1) / RUN;
+    const int64_t ntask = int64_t(nrun) * Nm1;
+    const Frag fi = ffs[1][lane];
+    const double2 si = sfs[4][lane];
+#pragma unroll 1
+    for (int64_t task = int64_t(blockIdx.x) * (NT / 32) + warp; task < ntask; task += int64_t(gridDim.x) * (NT / 32)) {
+      const int vy = 1 + int(task / nrun), vx0 = 1 + int(task % nrun) * RUN;
+      const int vx1 = min(vx0 + RUN, Nm1 + 1);
+      const int vary = vy == 1 ? 0 : (vy == Nm1 ? 2 : 1);
+      int64_t po = int64_t((vy - 1) * K + g) * n + (vx0 - 1) * K + 2 * q;
+      double b0 = r0 ? __ldg(r + po) : 0.0, b1 = r1 ? __ldg(r + po + 1) : 0.0;
+#pragma unroll 1
+      for (int vx = vx0; vx < vx1; ++vx) {
+        double nb0 = 0.0, nb1 = 0.0;
+        if (vx + 1 < vx1) {
+          nb0 = r0 ? __ldg(r + po + K) : 0.0;
+          nb1 = r1 ? __ldg(r + po + K + 1) : 0.0;
+        }
+        double u0, u1;
+        if (vary == 1 && vx != 1 && vx != Nm1) {
+          patch_solve(fi, fi, si, b0, b1, u0, u1);
+        } else {
+          const int varx = vx == 1 ? 0 : (vx == Nm1 ? 2 : 1);
+          patch_solve(ffs[varx][lane], ffs[vary][lane], sfs[varx * 3 + vary][lane], b0, b1, u0, u1);
+        }
+        double* xp = P.x + po;
+        if (r0) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp), "d"(u0) : "memory");
+        if (r1) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp + 1), "d"(u1) : "memory");
+        po += K;
+        b0 = nb0;
+        b1 = nb1;
+      }
+    }
+    return;
+  }
   // software pipeline: the next patch's coordinates and r fragment are loaded before this patch's
   // DMMA chain runs (the r loads are the latency the warps otherwise wait on)
   struct Item {
