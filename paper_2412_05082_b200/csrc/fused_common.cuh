@@ -35,6 +35,7 @@ struct ApplyP {
   int zero;                 // 0 at run time (opaque to the compiler)
   int64_t row0, lrows;      // slab window: local row 0 = global interior row row0; lrows rows held
   int64_t out_lo, out_hi;   // node rows j (= interior row + 1) to write, [out_lo, out_hi)
+  int chunk;                // apply2d: tile rows per column chunk
 };
 
 template <typename T, int K>

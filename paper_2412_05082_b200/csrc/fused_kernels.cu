@@ -103,59 +103,92 @@ struct ApplyLayout {
   static constexpr int BW = (C + 3) * K + 1;       // box: nodes [(c0-2)K, (c0+C+1)K]
   static constexpr int PX = odd(BW), PO = odd(O);
   static constexpr int XB = BW * PX, BB = O * PO;  // box, b tile
+  static constexpr int XN = O * PX;                // the O new box rows of a tile below the previous one
   static constexpr int STAGE = BW * PO;            // one of the three x-stage outputs
-  static constexpr int TOTAL = 2 * (XB + BB) + 3 * STAGE;
+  static constexpr int TOTAL = XB + 2 * XN + 2 * BB + 3 * STAGE;
   static constexpr int RBX = pick_rb(BW, C, RB), RBY = pick_rb(O, C, RB);
+  static constexpr int RBXN = pick_rb(O, C, RB);   // x-stage on the O new rows only
+  static_assert(BW - O <= O, "carried rows must not overlap the rows they are copied from");
   static constexpr int GX = cdiv(BW, RBX);         // row groups of the x-stage
   static constexpr int GY = cdiv(O, RBY);          // column groups of the y-stage
 };
 
 template <typename T, int K>
 __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__ ApplyP<T, K> P) {
+  // Work item = (tile column tx, chunk of CH tile rows): the CTA walks down the chunk.  Consecutive
+  // tiles of a column share BW - O box rows; their x-stage outputs are carried over (shifted up in
+  // shared memory), so only the O new box rows are loaded and contracted per tile after the first.
   using LY = ApplyLayout<T, K>;
   constexpr int C = LY::C, O = LY::O, BW = LY::BW, PX = LY::PX, PO = LY::PO;
-  constexpr int GX = LY::GX, GY = LY::GY;
+  const int CH = P.chunk;                        // tiles per column chunk (host: ~8 items per CTA)
+  constexpr int GY = LY::GY;
   constexpr int NT = 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  T* const xbuf0 = sm;                           // [2][XB]
-  T* const bbuf0 = sm + 2 * LY::XB;              // [2][BB]
-  T* sB = sm + 2 * (LY::XB + LY::BB);
+  T* const xfull = sm;                           // [XB]   full box of a chunk's first tile
+  T* const xnew0 = sm + LY::XB;                  // [2][XN] new rows of the following tiles
+  T* const bbuf0 = xnew0 + 2 * LY::XN;           // [2][BB]
+  T* sB = bbuf0 + 2 * LY::BB;
   T* sL = sB + LY::STAGE;
   T* sM = sL + LY::STAGE;
   const int64_t N = P.N, n = P.n, KN = K * N;
   const int ntx = int((N + C - 1) / C);
   int ty0, ty1;
   tile_rows<K, C>(P.out_lo, P.out_hi, ty0, ty1);
-  const int ntiles = ntx * (ty1 - ty0);
+  const int nch = (ty1 - ty0 + CH - 1) / CH;
+  const int nitems = ntx * nch;
   const int tid = threadIdx.x;
+  int round = 0;
 
-  auto issue = [&](int t, int buf) {
-    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(ty0 + t / ntx) * C;
-    load_box_async<T, BW, BW, PX>(xbuf0 + buf * LY::XB, P.x, n, KN, (cy0 - 2) * K, (cx0 - 2) * K, P.row0, P.lrows);
+  auto load_b = [&](int64_t cx0, int64_t cy0, int buf) {
     if (P.b) load_box_async<T, O, O, PO>(bbuf0 + buf * LY::BB, P.b, n, KN, cy0 * K, cx0 * K, P.row0, P.lrows);
   };
+  auto load_new = [&](int64_t cx0, int64_t cy0, int buf) {   // box rows [BW - O, BW) of tile row cy0
+    load_box_async<T, O, BW, PX>(xnew0 + buf * LY::XN, P.x, n, KN, (cy0 - 2) * K + (BW - O), (cx0 - 2) * K,
+                                 P.row0, P.lrows);
+  };
 
-  int buf = 0, round = 0;
-  if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
-  cp_async_commit();
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    if (t + (int)gridDim.x < ntiles) issue(t + gridDim.x, buf ^ 1);
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int tx = item % ntx, ch = item / ntx;
+    const int tA = ty0 + ch * CH, tB = min(tA + CH, ty1);
+    const int64_t cx0 = int64_t(tx) * C;
+    // first tile of the chunk: full box (synchronous), b tile
+    load_box_async<T, BW, BW, PX>(xfull, P.x, n, KN, (int64_t(tA) * C - 2) * K, (cx0 - 2) * K, P.row0, P.lrows);
+    load_b(cx0, int64_t(tA) * C, 0);
     cp_async_commit();
-    cp_async_wait1();
-    __syncthreads();
-    const T* xb = xbuf0 + buf * LY::XB;
-    const T* bt = bbuf0 + buf * LY::BB;
-    const int64_t cx0 = int64_t(t % ntx) * C, cy0 = int64_t(ty0 + t / ntx) * C;
-
+    int buf = 0;
+    for (int ty = tA; ty < tB; ++ty) {
+      const bool first = (ty == tA);
+      if (ty + 1 < tB) {                       // prefetch the next tile's new rows and b tile
+        load_new(cx0, int64_t(ty + 1) * C, buf ^ 1);
+        load_b(cx0, int64_t(ty + 1) * C, buf ^ 1);
+      }
+      cp_async_commit();
+      cp_async_wait1();
+      if (!first) {                            // carry the x-stage rows shared with the previous tile
+        for (int e = tid; e < (BW - O) * O; e += NT) {
+          const int r = e / O, cc = e - (e / O) * O;
+          const T vb = sB[(r + O) * PO + cc], vl = sL[(r + O) * PO + cc], vm = sM[(r + O) * PO + cc];
+          sB[r * PO + cc] = vb;
+          sL[r * PO + cc] = vl;
+          sM[r * PO + cc] = vm;
+        }
+      }
+      __syncthreads();
+      const T* xsrc = first ? xfull : xnew0 + buf * LY::XN;
+      const T* bt = bbuf0 + buf * LY::BB;
+      const int64_t cy0 = int64_t(ty) * C;
     const bool tin = (cx0 >= 2 && cx0 + C - 1 <= N - 2 && cy0 >= 2 && cy0 + C - 1 <= N - 2);
     auto tile_body = [&](auto INC) {
       constexpr bool IN = decltype(INC)::value;
-    // x-stage: B^_x x, L^_x x, M^_x x on all box rows, owned columns.  lanes <-> row groups;
-    // a thread holds rows g, g + GX, ... (RB rows) of one cell and reuses every coefficient RB times.
+    // x-stage: B^_x x, L^_x x, M^_x x on box rows [BW - NR, BW), owned columns.  lanes <-> row
+    // groups; a thread holds rows g, g + GX, ... (RB rows) of one cell and reuses every coefficient
+    // RB times.  x rows come from xsrc (local row = box row - (BW - NR)).
+    auto xstage = [&](auto NRC, auto RBC) {
+    constexpr int NR = decltype(NRC)::value, RB = decltype(RBC)::value;
+    constexpr int GX = cdiv(NR, RB), R0 = BW - NR;
 #pragma unroll 1
     for (int it = 0; it < cdiv(GX * C, NT); ++it, ++round) {
-      constexpr int RB = LY::RBX;
       const int u = it * NT + tid;
       if (u >= GX * C) continue;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
@@ -165,9 +198,9 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
       T w[RB][4 * K + 1];
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        const int row = min(g + r * GX, BW - 1);
+        const int lrow = min(g + r * GX, NR - 1);
 #pragma unroll
-        for (int q = 0; q <= 4 * K; ++q) w[r][q] = xb[row * PX + ci * K + q];
+        for (int q = 0; q <= 4 * K; ++q) w[r][q] = xsrc[lrow * PX + ci * K + q];
       }
       const bool inner = IN || (cx >= 2 && cx <= N - 2);
       if (inner) {
@@ -177,8 +210,8 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
         for (int p = 0; p < K; ++p)
 #pragma unroll
           for (int r = 0; r < RB; ++r) {
-            const int row = g + r * GX;
-            if (row < BW) {
+            const int row = R0 + g + r * GX;
+            if (g + r * GX < NR) {
               sB[row * PO + ci * K + p] = ob[p][r];
               sL[row * PO + ci * K + p] = ol[p][r];
               sM[row * PO + ci * K + p] = om[p][r];
@@ -206,8 +239,8 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
         });
 #pragma unroll
         for (int r = 0; r < RB; ++r) {
-          const int row = g + r * GX;
-          if (row < BW) {
+          const int row = R0 + g + r * GX;
+          if (g + r * GX < NR) {
             sB[row * PO + ci * K + p] = ob[r];
             sL[row * PO + ci * K + p] = ol[r];
             sM[row * PO + ci * K + p] = om[r];
@@ -215,6 +248,9 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
         }
       }
     }
+    };
+    if (first) xstage(std::integral_constant<int, BW>{}, std::integral_constant<int, LY::RBX>{});
+    else xstage(std::integral_constant<int, O>{}, std::integral_constant<int, LY::RBXN>{});
     __syncthreads();
 
     // y-stage: y = h^-2 (B^_y (M^_x x) + M^_y (B^_x x) + 2 L^_y (L^_x x)).  lanes <-> column
@@ -336,6 +372,7 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
     else tile_body(std::false_type{});
     __syncthreads();
     buf ^= 1;
+    }
   }
 }
 
@@ -1010,7 +1047,11 @@ static void launch_apply(const FusedLevel& F, const T* x, const T* b, T* y, cons
   p.row0 = w.row0; p.lrows = w.lrows; p.out_lo = w.out_lo; p.out_hi = w.out_hi;
   const int64_t ntx = (F.N + LY::C - 1) / LY::C;
   const int64_t nty = ((w.out_hi - 1) / K) / LY::C - (w.out_lo / K) / LY::C + 1;
-  const int grid = (int)std::min<int64_t>(grid_cache, ntx * nty);
+  // ~8 column chunks per CTA (static balance), each as tall as possible
+  const int64_t want = std::max<int64_t>(1, (8 * int64_t(grid_cache) + ntx - 1) / ntx);
+  p.chunk = int(std::max<int64_t>(1, (nty + want - 1) / want));
+  const int64_t nch = (nty + p.chunk - 1) / p.chunk;
+  const int grid = (int)std::min<int64_t>(grid_cache, ntx * nch);
   apply2d_kernel<T, K><<<grid, 256, smem, st>>>(p);
 }
 
