@@ -288,6 +288,7 @@ struct Fdm3P {
   int64_t count;
   int vlo[3], vcnt[3], vstr;
   unsigned mag[2];          // floor((2^32 - 1) / d) for d = vcnt[0], vcnt[1] (list mode: N - 1, (N - 1)^2)
+  int zc, zpar;             // zrun: patches per z chunk, parity of the chunks of this launch
   int64_t N, n;
   int64_t row0, lrows;      // slab window along z (see SlabWindow); the full domain: 0, n
   int64_t out_lo, out_hi;   // node planes written
@@ -617,6 +618,166 @@ __global__ void __launch_bounds__(256, 3) patch_fdm3d_kernel(const __grid_consta
     };
     if (inner) patch(std::true_type{});
     else patch(std::false_type{});
+  }
+}
+
+// ----------------------------------------------------------------------------- patch_fdm3d_zrun
+// Deterministic additive FDM update without atomics: one warp per patch column (vx, vy) of one x-y
+// parity class (columns of a class are disjoint in x and y), walking the patches of the column along
+// z.  Consecutive patches of a column overlap in k - 1 node planes: each patch's correction is added
+// to a per-warp ring of node planes in shared memory, and the k planes no later patch touches are
+// flushed to x with a plain read-modify-write (owned planes only).  Every DoF is written once per
+// class launch (4 launches per AVS step instead of 8 parity classes).
+template <typename T, int K>
+__global__ void __launch_bounds__(256, 3) patch_fdm3d_zrun_kernel(const __grid_constant__ Fdm3P<T, K> P) {
+  using LY = Fdm3Layout<T, K>;
+  constexpr int NP = LY::NP, NL2 = LY::NL2, LPL = LY::LPL;
+  constexpr int RING = 2 * K;                         // node planes held per warp (>= NP)
+  constexpr int WB = LY::WB + RING * NL2;             // FDM buffer | plane ring [RING][NP][NP]
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* const tab = reinterpret_cast<T*>(smem_raw) + 8 * WB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T* const buf = reinterpret_cast<T*>(smem_raw) + warp * WB;
+  T* const ring = buf + LY::WB;
+  for (int e = tid; e < LY::NL; e += 256) {
+    const int i = e % NP, j = (e / NP) % NP, m = e / NL2;
+    tab[e] = T(1) / (P.c.lam[1][i] + P.c.lam[1][j] + P.c.lam[1][m]);
+  }
+  for (int e = lane; e < RING * NL2; e += 32) ring[e] = T(0);
+  __syncthreads();
+  const int64_t N = P.N, n = P.n;
+  constexpr bool REGS = K <= 3;
+  T Sr[REGS ? NP * NP : 1];
+#pragma unroll
+  for (int e = 0; e < (REGS ? NP * NP : 1); ++e) Sr[e] = P.c.S[1][e];
+  // work item = (column of the class, z chunk of this launch's parity); chunks of one launch are
+  // separated by a chunk of the other parity, so their planes never overlap
+  // chunks are aligned to absolute vertex planes (chunk k: vz in [1 + k zc, 1 + (k+1) zc)), so a slab
+  // run splits its columns exactly where the full-domain run does (bitwise-equal owned planes)
+  const int ncol = P.vcnt[0] * P.vcnt[1];
+  const int zlo = P.vlo[2], zhi = P.vlo[2] + P.vcnt[2] - 1;
+  const int k0 = (zlo - 1) / P.zc, k1 = (zhi - 1) / P.zc;
+  const int kf = k0 + ((k0 & 1) != P.zpar ? 1 : 0);  // first chunk of parity zpar
+  const int nck = kf > k1 ? 0 : (k1 - kf) / 2 + 1;
+  const int nitem = ncol * nck;
+  const int stride = int(gridDim.x) * 8, first = int(blockIdx.x) * 8;
+  const int iters = nitem > first ? (nitem - first + stride - 1) / stride : 0;
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+    const int item = first + warp + it * stride;
+    if (item >= nitem) continue;
+    const int col = item % ncol, ck = kf + 2 * (item / ncol);
+    const int vz_a = max(1 + ck * P.zc, zlo), vz_b = min(1 + (ck + 1) * P.zc, zhi + 1);
+    const int vx = P.vlo[0] + P.vstr * (col % P.vcnt[0]), vy = P.vlo[1] + P.vstr * (col / P.vcnt[0]);
+    const int varx = variant_of(vx, N), vary = variant_of(vy, N);
+    const int64_t gxy = int64_t(vy - 1) * K * n + int64_t(vx - 1) * K;   // in-plane offset of the patch corner
+    auto flush = [&](int64_t jz, int slot) {          // node plane jz from ring slot: x += omega h acc
+      const bool own = jz >= P.out_lo && jz < P.out_hi;
+      T* xs = P.x + (jz - 1 - P.row0) * n * n + gxy;
+#pragma unroll 1
+      for (int e = lane; e < NL2; e += 32) {
+        const int xi = e % NP, yi = e / NP;
+        T* xp = xs + int64_t(yi) * n + xi;
+        T& a = ring[slot * NL2 + e];
+        if (own) *xp = fma(P.factor, a, *xp);
+        a = T(0);
+      }
+    };
+#pragma unroll 1
+    for (int vz = vz_a; vz < vz_b; ++vz) {
+      const int varz = variant_of(vz, N);
+      const int64_t g0 = (int64_t(vz - 1) * K - P.row0) * n * n + gxy;
+      const int64_t jz0 = int64_t(vz - 1) * K + 1;
+      T w[NP], o[NP];
+      const bool inner = (varx == 1 && vary == 1 && varz == 1);
+      auto patch = [&](auto INC) {
+        constexpr bool INNER = decltype(INC)::value;
+        const Coef2<T, K>& c0 = coef_at(P.c, (it * 8 + 0) * P.zero);
+#pragma unroll 1
+        for (int s = 0; s < LPL; ++s) {
+          const int ll = lane + 32 * s, la = ll % NP, lb = ll / NP;
+          if (ll >= NL2) continue;
+          const T* rp = P.r + g0 + (int64_t(lb) * n + la) * n;
+#pragma unroll
+          for (int l = 0; l < NP; ++l) w[l] = rp[l];
+          if constexpr (INNER && REGS) sdot_reg<T, K, true>(Sr, w, o); else sdot_var<T, K, true>(c0, varx, w, o);
+#pragma unroll
+          for (int i = 0; i < NP; ++i) buf[(lb * NP + la) * NP + i] = o[i];
+        }
+        __syncwarp();
+        const Coef2<T, K>& c1 = coef_at(P.c, (it * 8 + 1) * P.zero);
+#pragma unroll 1
+        for (int s = 0; s < LPL; ++s) {
+          const int ll = lane + 32 * s, la = ll % NP, lb = ll / NP;
+          if (ll >= NL2) continue;
+#pragma unroll
+          for (int l = 0; l < NP; ++l) w[l] = buf[(lb * NP + l) * NP + la];
+          if constexpr (INNER && REGS) sdot_reg<T, K, true>(Sr, w, o); else sdot_var<T, K, true>(c1, vary, w, o);
+#pragma unroll
+          for (int j = 0; j < NP; ++j) buf[(lb * NP + j) * NP + la] = o[j];
+        }
+        __syncwarp();
+        const Coef2<T, K>& c2 = coef_at(P.c, (it * 8 + 2) * P.zero);
+#pragma unroll 1
+        for (int s = 0; s < LPL; ++s) {
+          const int ll = lane + 32 * s, la = ll % NP, lb = ll / NP;
+          if (ll >= NL2) continue;
+#pragma unroll
+          for (int l = 0; l < NP; ++l) w[l] = buf[(l * NP + lb) * NP + la];
+          if constexpr (INNER && REGS) sdot_reg<T, K, true>(Sr, w, o); else sdot_var<T, K, true>(c2, varz, w, o);
+          if (INNER) {
+#pragma unroll
+            for (int m = 0; m < NP; ++m) o[m] *= tab[(m * NP + lb) * NP + la];
+          } else {
+            const T lxy = P.c.lam[varx][la] + P.c.lam[vary][lb];
+#pragma unroll
+            for (int m = 0; m < NP; ++m) o[m] /= (lxy + P.c.lam[varz][m]);
+          }
+          if constexpr (INNER && REGS) sdot_reg<T, K, false>(Sr, o, w); else sdot_var<T, K, false>(c2, varz, o, w);
+#pragma unroll
+          for (int m = 0; m < NP; ++m) buf[(m * NP + lb) * NP + la] = w[m];
+        }
+        __syncwarp();
+        const Coef2<T, K>& c3 = coef_at(P.c, (it * 8 + 3) * P.zero);
+#pragma unroll 1
+        for (int s = 0; s < LPL; ++s) {
+          const int ll = lane + 32 * s, la = ll % NP, lb = ll / NP;
+          if (ll >= NL2) continue;
+#pragma unroll
+          for (int l = 0; l < NP; ++l) w[l] = buf[(lb * NP + l) * NP + la];
+          if constexpr (INNER && REGS) sdot_reg<T, K, false>(Sr, w, o); else sdot_var<T, K, false>(c3, vary, w, o);
+#pragma unroll
+          for (int j = 0; j < NP; ++j) buf[(lb * NP + j) * NP + la] = o[j];
+        }
+        __syncwarp();
+        // S_x on x lines (y, z), accumulated into the plane ring
+        const Coef2<T, K>& c4 = coef_at(P.c, (it * 8 + 4) * P.zero);
+#pragma unroll 1
+        for (int s = 0; s < LPL; ++s) {
+          const int ll = lane + 32 * s, la = ll % NP, lb = ll / NP;
+          if (ll >= NL2) continue;
+#pragma unroll
+          for (int l = 0; l < NP; ++l) w[l] = buf[(lb * NP + la) * NP + l];
+          if constexpr (INNER && REGS) sdot_reg<T, K, false>(Sr, w, o); else sdot_var<T, K, false>(c4, varx, w, o);
+          T* rg = ring + int((jz0 + lb) % RING) * NL2 + la * NP;
+#pragma unroll
+          for (int i = 0; i < NP; ++i) rg[i] += o[i];
+        }
+        __syncwarp();
+      };
+      if (inner) patch(std::true_type{});
+      else patch(std::false_type{});
+      // planes jz0 .. jz0 + K - 1 are final (the next patch of the column starts at jz0 + K)
+#pragma unroll 1
+      for (int pz = 0; pz < K; ++pz) flush(jz0 + pz, int((jz0 + pz) % RING));
+      __syncwarp();
+    }
+    // the chunk's last patch's remaining NP - K planes (the next chunk, in the other launch, adds to
+    // them afterwards)
+    const int64_t jzl = int64_t(vz_b - 2) * K + 1 + K;
+#pragma unroll 1
+    for (int pz = 0; pz < NP - K; ++pz) flush(jzl + pz, int((jzl + pz) % RING));
+    __syncwarp();
   }
 }
 
@@ -1168,6 +1329,40 @@ bool fused3_patch_fdm(FusedLevel& F, T omega, const T* r, T* x, const int32_t* l
   return fdm3_dispatch<T>(F, omega, r, x, ps, atomic, full_window3(F), st, launches);
 }
 
+template <typename T, int K>
+static void launch_fdm3_zrun(const FusedLevel& F, T omega, const T* r, T* x, const PatchSet3& ps, const SlabWindow& w,
+                             int zc, int zpar, cudaStream_t st) {
+  using LY = Fdm3Layout<T, K>;
+  const size_t smem = sizeof(T) * size_t(8 * (LY::WB + 2 * K * LY::NL2) + LY::NL);
+  static int grid_cache = -1;
+  if (grid_cache < 0) {
+    cudaFuncSetAttribute(patch_fdm3d_zrun_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, patch_fdm3d_zrun_kernel<T, K>, 256, smem);
+    grid_cache = sms * std::max(per, 1);
+  }
+  Fdm3P<T, K> p;
+  std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
+  p.r = r; p.x = x; p.list = nullptr; p.count = 0; p.N = F.N; p.n = F.n;
+  for (int a = 0; a < 3; ++a) { p.vlo[a] = ps.vlo[a]; p.vcnt[a] = ps.vcnt[a]; }
+  p.vstr = ps.vstr;
+  p.mag[0] = p.mag[1] = 0;
+  p.row0 = w.row0; p.lrows = w.lrows; p.out_lo = w.out_lo; p.out_hi = w.out_hi;
+  p.factor = T(double(omega) * F.h);
+  p.zero = 0;
+  p.atomic = 0;
+  p.zc = zc;
+  p.zpar = zpar;
+  const int64_t cols = int64_t(ps.vcnt[0]) * ps.vcnt[1];
+  const int zlo = ps.vlo[2], zhi = ps.vlo[2] + ps.vcnt[2] - 1, k0 = (zlo - 1) / zc, k1 = (zhi - 1) / zc;
+  const int kf = k0 + ((k0 & 1) != zpar ? 1 : 0);
+  const int64_t nck = kf > k1 ? 0 : (k1 - kf) / 2 + 1;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid_cache, (cols * nck + 7) / 8));
+  if (cols * nck > 0) patch_fdm3d_zrun_kernel<T, K><<<grid, 256, smem, st>>>(p);
+}
+
 template <typename T>
 bool fused3_fdm_window(FusedLevel& F, T omega, const T* r, T* x, bool atomic, cudaStream_t st, int64_t* launches,
                        const SlabWindow* win) {
@@ -1186,6 +1381,37 @@ bool fused3_fdm_window(FusedLevel& F, T omega, const T* r, T* x, bool atomic, cu
     ps.vcnt[2] = vz_hi - vz_lo + 1;
     ps.count = int64_t(Nm1) * Nm1 * ps.vcnt[2];
     return fdm3_dispatch<T>(F, omega, r, x, ps, 1, w, st, launches);
+  }
+  // deterministic: 4 x-y parity classes of patch columns, each column walked along z (zrun kernel)
+  if (K <= 5 && !std::getenv("C0IP_NO_ZRUN")) {
+    for (int c = 0; c < 4; ++c) {
+      PatchSet3 ps;
+      ps.vstr = 2;
+      int cnt = 1;
+      for (int a = 0; a < 2; ++a) {
+        const int par = (c >> a) & 1;
+        const int v0 = 1 + ((1 & 1) != par ? 1 : 0);
+        ps.vlo[a] = v0;
+        ps.vcnt[a] = v0 > Nm1 ? 0 : (Nm1 - v0) / 2 + 1;
+        cnt *= ps.vcnt[a];
+      }
+      ps.vlo[2] = vz_lo;
+      ps.vcnt[2] = vz_hi - vz_lo + 1;
+      if (cnt == 0) continue;
+      // z chunks of ZC patches, even and odd chunks in two launches (~8 warp waves per launch)
+      constexpr int ZC = 8;
+      for (int zpar = 0; zpar < 2; ++zpar) {
+        switch (K) {
+          case 2: launch_fdm3_zrun<T, 2>(F, omega, r, x, ps, w, ZC, zpar, st); break;
+          case 3: launch_fdm3_zrun<T, 3>(F, omega, r, x, ps, w, ZC, zpar, st); break;
+          case 4: launch_fdm3_zrun<T, 4>(F, omega, r, x, ps, w, ZC, zpar, st); break;
+          case 5: launch_fdm3_zrun<T, 5>(F, omega, r, x, ps, w, ZC, zpar, st); break;
+        }
+        (*launches)++;
+        check3("fused patch_fdm3d_zrun launch");
+      }
+    }
+    return true;
   }
   // 2^3 parity classes (v_a mod 2), mutually disjoint patches: deterministic plain stores
   for (int c = 0; c < 8; ++c) {
