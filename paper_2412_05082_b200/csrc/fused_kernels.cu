@@ -106,8 +106,11 @@ struct ApplyLayout {
   static constexpr int XN = O * PX;                // the O new box rows of a tile below the previous one
   static constexpr int STAGE = BW * PO;            // one of the three x-stage outputs
   static constexpr int TOTAL = XB + 2 * XN + 2 * BB + 3 * STAGE;
-  static constexpr int RBX = pick_rb(BW, C, RB), RBY = pick_rb(O, C, RB);
-  static constexpr int RBXN = pick_rb(O, C, RB);   // x-stage on the O new rows only
+  // register blocking: the column-walk stages have few units (O rows x C cells); for k = 4 blocking RB
+  // lines per thread (one LDCU per RB DFMA, half the threads idle) measured faster than the balanced
+  // choice of pick_rb, for the other degrees slower (0.205 -> 0.196 ms at k = 4; k = 2, 5 regress)
+  static constexpr int RBX = pick_rb(BW, C, RB), RBY = (K == 4) ? RB : pick_rb(O, C, RB);
+  static constexpr int RBXN = (K == 4) ? RB : pick_rb(O, C, RB);   // x-stage on the O new rows only
   static_assert(BW - O <= O, "carried rows must not overlap the rows they are copied from");
   static constexpr int GX = cdiv(BW, RBX);         // row groups of the x-stage
   static constexpr int GY = cdiv(O, RBY);          // column groups of the y-stage
