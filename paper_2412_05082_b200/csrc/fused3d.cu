@@ -143,38 +143,56 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
     __syncthreads();
     const T* xb = xb0 + (s & 1) * LY::XB;
 
-    // x-stage: unit = (plane, box row, cell) -> B^ L^ M^ along x for the K nodes of the cell
+    // x-stage: unit = (plane, box row group, cell) -> B^ L^ M^ along x for the K nodes of the cell;
+    // rows hr, hr + HB, ... (XR rows) share every coefficient load (register blocking; XR = 1 for FP64
+    // k = 3, where the second row spills at the 2-CTA register budget -- measured)
+    {
+      constexpr int XR = (K == 3 && sizeof(T) == 8) ? 1 : 2;
+      constexpr int HB = cdiv(BW, XR);
 #pragma unroll 1
-    for (int it = 0; it < cdiv(K * BW * C, NT); ++it, ++round) {
-      const int u = it * NT + tid;
-      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
-      if (u >= K * BW * C) continue;
-      const int r = u % BW, rest = u / BW, ci = rest % C, pz = rest / C;
-      const int64_t cx = cx0 + ci;
-      if (cx >= N) continue;
-      T w[1][4 * K + 1];
+      for (int it = 0; it < cdiv(K * HB * C, NT); ++it, ++round) {
+        const int u = it * NT + tid;
+        const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+        if (u >= K * HB * C) continue;
+        const int hr = u % HB, rest = u / HB, ci = rest % C, pz = rest / C;
+        const int64_t cx = cx0 + ci;
+        if (cx >= N) continue;
+        int rr[XR];
 #pragma unroll
-      for (int q = 0; q <= 4 * K; ++q) w[0][q] = xb[(pz * BW + r) * PX + ci * K + q];
-      const bool inner = (cx >= 2 && cx <= N - 2);
+        for (int j = 0; j < XR; ++j) rr[j] = min(hr + j * HB, BW - 1);
+        T w[XR][4 * K + 1];
 #pragma unroll
-      for (int p = 0; p < K; ++p) {
-        T ob[1] = {0}, ol[1] = {0}, om[1] = {0};
-        const int sp = inner ? -1 : special_row<K>(cx * K + p, N);
-        with_p<K>(p, [&](auto PC) {
-          constexpr int PP = decltype(PC)::value;
-          if (sp < 0) {
-            rowB<T, K, PP>([&](int q) { return c.BI[PP][q]; }, w, 0, ob);
-            rowML<T, K, PP>([&](int q) { return c.LI[PP][q]; }, w, K, ol);
-            rowML<T, K, PP>([&](int q) { return c.MI[PP][q]; }, w, K, om);
-          } else {
-            rowB<T, K, PP>([&](int q) { return c.BS[sp][q]; }, w, 0, ob);
-            rowML<T, K, PP>([&](int q) { return c.LS[sp][q + K]; }, w, K, ol);
-            rowML<T, K, PP>([&](int q) { return c.MS[sp][q + K]; }, w, K, om);
+        for (int j = 0; j < XR; ++j)
+#pragma unroll
+          for (int q = 0; q <= 4 * K; ++q) w[j][q] = xb[(pz * BW + rr[j]) * PX + ci * K + q];
+        const bool inner = (cx >= 2 && cx <= N - 2);
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          T ob[XR], ol[XR], om[XR];
+#pragma unroll
+          for (int j = 0; j < XR; ++j) ob[j] = ol[j] = om[j] = T(0);
+          const int sp = inner ? -1 : special_row<K>(cx * K + p, N);
+          with_p<K>(p, [&](auto PC) {
+            constexpr int PP = decltype(PC)::value;
+            if (sp < 0) {
+              rowB<T, K, PP>([&](int q) { return c.BI[PP][q]; }, w, 0, ob);
+              rowML<T, K, PP>([&](int q) { return c.LI[PP][q]; }, w, K, ol);
+              rowML<T, K, PP>([&](int q) { return c.MI[PP][q]; }, w, K, om);
+            } else {
+              rowB<T, K, PP>([&](int q) { return c.BS[sp][q]; }, w, 0, ob);
+              rowML<T, K, PP>([&](int q) { return c.LS[sp][q + K]; }, w, K, ol);
+              rowML<T, K, PP>([&](int q) { return c.MS[sp][q + K]; }, w, K, om);
+            }
+          });
+#pragma unroll
+          for (int j = 0; j < XR; ++j) {
+            if (hr + j * HB >= BW) continue;
+            const int r = rr[j];
+            sx[((pz * 3 + 0) * BW + r) * PO + ci * K + p] = ob[j];
+            sx[((pz * 3 + 1) * BW + r) * PO + ci * K + p] = ol[j];
+            sx[((pz * 3 + 2) * BW + r) * PO + ci * K + p] = om[j];
           }
-        });
-        sx[((pz * 3 + 0) * BW + r) * PO + ci * K + p] = ob[0];
-        sx[((pz * 3 + 1) * BW + r) * PO + ci * K + p] = ol[0];
-        sx[((pz * 3 + 2) * BW + r) * PO + ci * K + p] = om[0];
+        }
       }
     }
     __syncthreads();
