@@ -160,6 +160,20 @@ c0ip_status c0ip_pcg(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, do
                      double rtol, int32_t max_iter, c0ip_report* rep, double* res_history,
                      void* stream);
 
+/* MG-preconditioned flexible GMRES(m) in FP64 (GMRES is the paper's
+ * outer solver for the multiplicative smoother, whose same-order V-cycle (mg->symmetric = 0) is not
+ * symmetric).  Right preconditioning z_j = MG(v_j) (c0ip_vcycle), modified Gram-Schmidt Arnoldi,
+ * Givens rotations, restart after `restart` steps (the device holds restart+1 Krylov vectors and
+ * restart preconditioned vectors of the finest level: (2 restart + 2) * 8 n bytes, owned by the ctx).
+ * x (device FP64, in: x0, out: solution), b device FP64.  Stops when the least-squares residual
+ * |g_{j+1}| <= rtol ||r_0|| (a restart cycle follows while the true residual is above the tolerance) or
+ * after max_iter Arnoldi steps (not an error: converged = 0).
+ * rep->rn is the true residual norm ||b - A x|| at exit; res_history (optional host array of
+ * max_iter+1 doubles) holds ||r_0||, |g_1|, ..., |g_n|.  ARG for restart < 1, max_iter < 0, rtol < 0. */
+c0ip_status c0ip_gmres(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, double* x,
+                       double rtol, int32_t max_iter, int32_t restart, c0ip_report* rep,
+                       double* res_history, void* stream);
+
 /* ---- Slab (multi-GPU) entry points, SURVEY.md §8e -------------------------------------------------
  * The mesh is split into slabs along the slowest axis (y in 2D, z in 3D); each rank (one process per
  * GPU) holds a window of global interior rows [row0, row0 + lrows) of that axis in a contiguous array

@@ -125,6 +125,63 @@ def pcg(A, b, prec, rtol=1e-8, max_iter=200, x0=None):
     return x, n, np.array(hist)
 
 
+def gmres(A, b, prec, rtol=1e-8, max_iter=200, restart=50, x0=None):
+    """Flexible right-preconditioned restarted GMRES, FGMRES(m) (Saad, Iterative Methods for Sparse
+    Linear Systems, Alg. 9.6; with a fixed preconditioner it is right-preconditioned GMRES, Alg. 9.5):
+    modified Gram-Schmidt Arnoldi on A M^{-1}, Givens rotations for the least-squares problem, x
+    updated from the stored preconditioned vectors Z at the end of every cycle.  PAPER.md:487 (GMRES
+    outer solver for the multiplicative smoother, rtol 1e-8 relative to ||r_0||).  Returns x,
+    iterations n (Arnoldi steps), history of the least-squares residual norms |g_{j+1}| (the true
+    residual norm in exact arithmetic)."""
+    x = np.zeros_like(b) if x0 is None else x0.copy()
+    r = b - A @ x
+    beta = np.linalg.norm(r)
+    hist = [beta]
+    r0 = beta
+    n = 0
+    # cycles continue until the TRUE residual meets the tolerance (the least-squares estimate |g| can
+    # undershoot it in finite precision); a cycle ends at |g_{j+1}| <= rtol r0 or after `restart` steps
+    while n < max_iter and beta > rtol * r0:
+        m = min(restart, max_iter - n)
+        V = [r / beta]
+        Z = []
+        H = np.zeros((m + 1, m))
+        cs, sn = np.zeros(m), np.zeros(m)
+        g = np.zeros(m + 1)
+        g[0] = beta
+        j_done = 0
+        for j in range(m):
+            z = prec(V[j])
+            Z.append(z)
+            w = A @ z
+            for i in range(j + 1):                     # modified Gram-Schmidt
+                H[i, j] = w @ V[i]
+                w = w - H[i, j] * V[i]
+            H[j + 1, j] = np.linalg.norm(w)
+            V.append(w / H[j + 1, j] if H[j + 1, j] > 0 else w)
+            for i in range(j):                         # apply the previous rotations
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            den = np.hypot(H[j, j], H[j + 1, j])
+            cs[j], sn[j] = H[j, j] / den, H[j + 1, j] / den
+            H[j, j] = den
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            n += 1
+            j_done = j + 1
+            hist.append(abs(g[j + 1]))
+            if hist[-1] <= rtol * r0:
+                break
+        y = np.linalg.solve(np.triu(H[:j_done, :j_done]), g[:j_done])
+        for i in range(j_done):
+            x = x + y[i] * Z[i]
+        r = b - A @ x
+        beta = np.linalg.norm(r)
+    return x, n, np.array(hist)
+
+
 def fractional_iterations(hist):
     """nu = -8 / log10(rbar), rbar = (||r_n||/||r_0||)^(1/n) (reading Q7)."""
     n = len(hist) - 1

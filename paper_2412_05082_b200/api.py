@@ -158,6 +158,17 @@ class Context:
                       seconds=rep.seconds)
         return x, report, hist[: rep.iterations + 1]
 
+    def gmres(self, mg, b, x=None, rtol=1e-8, max_iter=200, restart=50):
+        """Flexible right-preconditioned GMRES(restart) in FP64 around the V-cycle (c0ip_gmres)."""
+        x = torch.zeros_like(b) if x is None else x
+        rep = L.Report()
+        hist = np.zeros(max_iter + 1)
+        L.check(self._lib.c0ip_gmres(self.h, C.byref(mg.c), _ptr(b), _ptr(x), float(rtol), int(max_iter),
+                                     int(restart), C.byref(rep), hist.ctypes.data_as(C.c_void_p), _stream()))
+        report = dict(iterations=rep.iterations, converged=bool(rep.converged), r0=rep.r0, rn=rep.rn, nu=rep.nu,
+                      seconds=rep.seconds)
+        return x, report, hist[: rep.iterations + 1]
+
     # ------------------------------------------------------------------ slab (multi-GPU) calls
     def slab_ghosts(self):
         ga, gp = C.c_int32(), C.c_int32()

@@ -112,6 +112,9 @@ struct c0ip_ctx_s {
   std::vector<Level> levels;          // index = level number (entries < lmin unused)
   int64_t launches = 0;
   DevArr<double> pcg_r, pcg_z, pcg_p, pcg_Ap, dot_part, dot_out;
+  DevArr<double> gm_V, gm_Z, gm_w;                 // GMRES: Krylov basis, preconditioned basis, work
+  const double* vc_r = nullptr;                    // buffers the captured V-cycle graph reads / writes
+  double* vc_z = nullptr;
   double* dot_host = nullptr;
   // captured V-cycle (CUDA graph) for the PCG loop: key = mg config; replayed on the caller's stream
   cudaStream_t cap_stream = nullptr;
@@ -134,6 +137,7 @@ struct c0ip_ctx_s {
       L.fused.reset();
     }
     pcg_r.free(); pcg_z.free(); pcg_p.free(); pcg_Ap.free(); dot_part.free(); dot_out.free();
+    gm_V.free(); gm_Z.free(); gm_w.free();
     if (dot_host) cudaFreeHost(dot_host);
   }
 };
@@ -504,7 +508,10 @@ bool same_mg(const c0ip_mg_config& a, const c0ip_mg_config& b) {
 }
 
 void vcycle_graph(c0ip_ctx ctx, const c0ip_mg_config& mg, const double* r, double* z, cudaStream_t st) {
-  if (!ctx->vc_exec || !same_mg(ctx->vc_key, mg)) {
+  // the captured graph bakes in r and z: recapture if the config or the buffers change
+  if (!ctx->vc_exec || !same_mg(ctx->vc_key, mg) || ctx->vc_r != r || ctx->vc_z != z) {
+    ctx->vc_r = r;
+    ctx->vc_z = z;
     if (ctx->vc_exec) { cudaGraphExecDestroy(ctx->vc_exec); ctx->vc_exec = nullptr; }
     if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
     CK(cudaStreamSynchronize(st));
@@ -930,6 +937,113 @@ c0ip_status c0ip_pcg(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, do
     rep->r0 = r0;
     rep->rn = rn;
     double ratio = (r0 > 0) ? rn / r0 : 0.0;
+    rep->nu = (it == 0 || ratio <= 0) ? 0.0 : -8.0 / std::log10(std::pow(ratio, 1.0 / it));
+    rep->seconds = std::chrono::duration<double>(t1 - t0).count();
+  }
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_gmres(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, double* x, double rtol,
+                       int32_t max_iter, int32_t restart, c0ip_report* rep, double* res_history, void* stream) {
+  c0ip_status s = check_mg(ctx, mg);
+  if (s) return s;
+  if (!b || !x) return fail(C0IP_ERR_ARG, "null vector");
+  if (max_iter < 0 || restart < 1 || !(rtol >= 0)) return fail(C0IP_ERR_ARG, "bad rtol / max_iter / restart");
+  ABI_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  auto t0 = std::chrono::steady_clock::now();
+  Level& L = ctx->levels[ctx->lmax];
+  const int64_t n = L.ndofs;
+  const int m = std::max(1, std::min<int>(restart, std::max(1, max_iter)));
+  // Flexible right-preconditioned GMRES(m) (Saad Alg. 9.6), modified Gram-Schmidt, Givens rotations
+  // (GMRES outer solver for the multiplicative smoother)
+  ctx->gm_V.alloc(n * (m + 1));
+  ctx->gm_Z.alloc(n * m);
+  ctx->gm_w.alloc(n);
+  ctx->pcg_r.alloc(n);
+  ctx->pcg_z.alloc(n);
+  double* V = ctx->gm_V.p;
+  double* Z = ctx->gm_Z.p;
+  double* w = ctx->gm_w.p;
+  std::vector<double> H((m + 1) * m), cs(m), sn(m), g(m + 1), y(m);
+  auto h = [&](int i, int j) -> double& { return H[size_t(i) * m + j]; };
+  double dd[3];
+  auto residual_norm = [&]() {                       // V_0 = b - A x, returns ||V_0||
+    apply_op<double>(ctx, L, x, b, V, st);
+    dots(ctx, n, 1, V, V, nullptr, nullptr, nullptr, nullptr, dd, st);
+    return std::sqrt(dd[0]);
+  };
+  double beta = residual_norm();
+  const double r0 = beta;
+  double rn = beta;
+  if (res_history) res_history[0] = r0;
+  int it = 0;
+  // cycles continue until the TRUE residual meets the tolerance (the least-squares estimate |g| can
+  // undershoot it in finite precision)
+  while (it < max_iter && beta > rtol * r0) {
+    const int mm = std::min(m, max_iter - it);
+    axpby<double>(ctx, n, 0.0, b, 1.0 / beta, V, st);            // V_0 = r / beta
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int jd = 0;
+    for (int j = 0; j < mm; ++j) {
+      double* vj = V + size_t(j) * n;
+      double* zj = Z + size_t(j) * n;
+      // z_j = MG(v_j): the first application runs uncaptured (allocates the level workspaces), the
+      // rest replay the captured V-cycle graph on the fixed staging buffers pcg_r -> pcg_z
+      if (it == 0) {
+        vcycle_top(ctx, *mg, vj, zj, st);
+      } else {
+        CK(cudaMemcpyAsync(ctx->pcg_r.p, vj, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        vcycle_graph(ctx, *mg, ctx->pcg_r.p, ctx->pcg_z.p, st);
+        CK(cudaMemcpyAsync(zj, ctx->pcg_z.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      }
+      apply_op<double>(ctx, L, zj, nullptr, w, st);              // w = A z_j
+      for (int i = 0; i <= j; ++i) {                             // modified Gram-Schmidt
+        dots(ctx, n, 1, w, V + size_t(i) * n, nullptr, nullptr, nullptr, nullptr, dd, st);
+        h(i, j) = dd[0];
+        axpby<double>(ctx, n, -dd[0], V + size_t(i) * n, 1.0, w, st);
+      }
+      dots(ctx, n, 1, w, w, nullptr, nullptr, nullptr, nullptr, dd, st);
+      h(j + 1, j) = std::sqrt(dd[0]);
+      double* vn = V + size_t(j + 1) * n;
+      CK(cudaMemcpyAsync(vn, w, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      if (h(j + 1, j) > 0) axpby<double>(ctx, n, 0.0, w, 1.0 / h(j + 1, j), vn, st);
+      for (int i = 0; i < j; ++i) {                              // previous rotations
+        const double t = cs[i] * h(i, j) + sn[i] * h(i + 1, j);
+        h(i + 1, j) = -sn[i] * h(i, j) + cs[i] * h(i + 1, j);
+        h(i, j) = t;
+      }
+      const double den = std::hypot(h(j, j), h(j + 1, j));
+      cs[j] = h(j, j) / den;
+      sn[j] = h(j + 1, j) / den;
+      h(j, j) = den;
+      h(j + 1, j) = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++it;
+      jd = j + 1;
+      rn = std::fabs(g[j + 1]);
+      if (res_history) res_history[it] = rn;
+      if (rn <= rtol * r0) break;
+    }
+    for (int i = jd - 1; i >= 0; --i) {                          // back substitution H y = g
+      double t = g[i];
+      for (int l = i + 1; l < jd; ++l) t -= h(i, l) * y[l];
+      y[i] = t / h(i, i);
+    }
+    for (int i = 0; i < jd; ++i) axpby<double>(ctx, n, y[i], Z + size_t(i) * n, 1.0, x, st);
+    beta = residual_norm();                                       // true residual of the restart / exit
+  }
+  CK(cudaStreamSynchronize(st));
+  auto t1 = std::chrono::steady_clock::now();
+  if (rep) {
+    rep->iterations = it;
+    rep->converged = (beta <= rtol * r0) ? 1 : 0;
+    rep->r0 = r0;
+    rep->rn = beta;                                               // true residual norm at exit
+    const double ratio = (r0 > 0) ? rn / r0 : 0.0;
     rep->nu = (it == 0 || ratio <= 0) ? 0.0 : -8.0 / std::log10(std::pow(ratio, 1.0 / it));
     rep->seconds = std::chrono::duration<double>(t1 - t0).count();
   }

@@ -277,6 +277,45 @@ def test_pcg_iterations(d, k, L, sm, steps, om):
     ctx.close()
 
 
+@pytest.mark.parametrize("d,k,L,sm,steps,om,sym", [(2, 2, 3, "mvs", 1, 1.0, False), (2, 3, 4, "mvs", 1, 1.0, False),
+                                                   (2, 4, 5, "mvs", 1, 1.0, False), (2, 2, 4, "avs", 2, 0.25, True),
+                                                   (3, 2, 3, "mvs", 1, 0.7, False)])
+def test_gmres_iterations(d, k, L, sm, steps, om, sym):
+    """GMRES around the paper's same-order (nonsymmetric) MVS cycle:
+    iteration count within 1 (FP64 cycle) / 2 (FP32 cycle) of the oracle's FGMRES, true residual at
+    the tolerance, nu within 0.5."""
+    from paper_2412_05082_b200 import api
+    from oracle.multigrid import gmres
+    ctx = api.Context(d, k, L)
+    h = Hierarchy(k, d, L, default_sigma(k))
+    b = rhs_load(k, d, 2 ** L, paper_load(d))
+    xo, no, ho = gmres(h.A[L], b, lambda r: precondition(h, r, sm, steps, om, symmetric=sym))
+    for dt in (torch.float64, torch.float32):
+        x, rep, hist = ctx.gmres(api.MG(sm, steps, om, symmetric=sym, cycle_dtype=dt), torch.tensor(b, device=DEV))
+        assert rep["converged"]
+        assert abs(rep["iterations"] - no) <= (1 if dt == torch.float64 else 2), (rep["iterations"], no)
+        xn = x.cpu().numpy()
+        # the residual of a smooth solution is itself only known to ~ eps || |A| |x| || (SURVEY.md F9:
+        # cancellation 1e7..1e12); the GPU stops on its own residual, so the host-measured one is checked
+        # against the tolerance plus that rounding floor
+        tr = np.linalg.norm(b - h.A[L] @ xn) / np.linalg.norm(b)
+        floor = 32 * 2.2e-16 * np.linalg.norm(abs(h.A[L]) @ np.abs(xn)) / np.linalg.norm(b)
+        assert tr <= 1.05e-8 + floor, (dt, tr, floor, rep, hist[-3:], ho[-3:])
+        if dt == torch.float64:
+            assert abs(rep["nu"] - fractional_iterations(ho)) <= 0.5
+            assert np.allclose(hist[: min(len(hist), len(ho))], ho[: min(len(hist), len(ho))], rtol=1e-6, atol=1e-12 * ho[0])
+    ctx.close()
+
+
+def test_gmres_bad_restart_is_arg_error():
+    from paper_2412_05082_b200 import api
+    ctx = api.Context(2, 2, 3)
+    b = torch.zeros(ctx.n_dofs(3), device=DEV, dtype=torch.float64)
+    with pytest.raises(Exception):
+        ctx.gmres(api.MG("mvs", 1, 1.0), b, restart=0)
+    ctx.close()
+
+
 def test_coercivity_error():
     from paper_2412_05082_b200 import api, _lib
     with pytest.raises(_lib.C0ipError) as e:

@@ -117,3 +117,59 @@ def test_two_grid_h_independent():
         b = rhs_load(k, 2, level_cells(L), paper_load(2))
         nus.append(fractional_iterations(pcg(A, b, tg)[2]))
     assert abs(nus[1] - nus[0]) < 1.5 and nus[1] < 20
+
+
+# ------------------------------------------------------------------------------ GMRES
+def test_gmres_matches_direct_solve_and_is_monotone():
+    """Textbook properties: the solution of a small nonsymmetric system (np.linalg.solve), and the
+    minimal-residual property -- the residual history never increases within a cycle."""
+    from oracle.multigrid import gmres
+    rng = np.random.default_rng(3)
+    n = 40
+    A = np.eye(n) * 4 + rng.standard_normal((n, n)) * 0.3
+    b = rng.standard_normal(n)
+    x, it, hist = gmres(A, b, lambda v: v, rtol=1e-12, max_iter=200, restart=60)
+    assert np.linalg.norm(x - np.linalg.solve(A, b)) <= 1e-10 * np.linalg.norm(np.linalg.solve(A, b))
+    assert np.all(np.diff(hist[:it + 1]) <= 1e-12 * hist[0])
+    assert np.linalg.norm(b - A @ x) <= 1e-11 * np.linalg.norm(b)
+
+
+def test_gmres_terminates_in_number_of_distinct_eigenvalues():
+    """Krylov theory: for a diagonalisable A with m distinct eigenvalues GMRES (no restart) reaches
+    the exact solution in at most m steps."""
+    from oracle.multigrid import gmres
+    rng = np.random.default_rng(4)
+    Q, _ = np.linalg.qr(rng.standard_normal((30, 30)))
+    lam = np.repeat([1.0, 2.5, 7.0, 11.0], [10, 8, 7, 5])
+    A = Q @ np.diag(lam) @ Q.T
+    b = rng.standard_normal(30)
+    x, it, hist = gmres(A, b, lambda v: v, rtol=1e-13, max_iter=30, restart=30)
+    assert it <= 4
+    assert np.linalg.norm(b - A @ x) <= 1e-11 * np.linalg.norm(b)
+
+
+def test_gmres_right_preconditioning_exact_inverse():
+    """With M^{-1} = A^{-1} right-preconditioned GMRES converges in one step."""
+    from oracle.multigrid import gmres
+    rng = np.random.default_rng(5)
+    A = np.eye(20) * 3 + rng.standard_normal((20, 20)) * 0.5
+    Ai = np.linalg.inv(A)
+    b = rng.standard_normal(20)
+    x, it, hist = gmres(A, b, lambda v: Ai @ v, rtol=1e-12)
+    assert it == 1
+    assert np.allclose(x, np.linalg.solve(A, b), rtol=1e-10, atol=1e-12)
+
+
+def test_gmres_with_nonsymmetric_mvs_cycle_solves_cfg1():
+    """The paper's MVS protocol: GMRES around the same-order (nonsymmetric) MVS V-cycle
+    on cfg1 reaches the direct solution; its iteration count is level-independent-ish and small."""
+    from oracle.multigrid import gmres, Hierarchy, precondition
+    h = Hierarchy(2, 2, 3, default_sigma(2))
+    A = h.A[3]
+    rng = np.random.default_rng(6)
+    b = rng.standard_normal(A.shape[0])
+    prec = lambda r: precondition(h, r, "mvs", 1, 1.0, symmetric=False)
+    x, it, hist = gmres(A, b, prec, rtol=1e-10)
+    xd = np.linalg.solve(A.toarray(), b)
+    assert np.linalg.norm(x - xd) <= 1e-8 * np.linalg.norm(xd)
+    assert it <= 15
