@@ -166,7 +166,7 @@ c0ip_status c0ip_pcg(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, do
  * Givens rotations, restart after `restart` steps (the device holds restart+1 Krylov vectors and
  * restart preconditioned vectors of the finest level: (2 restart + 2) * 8 n bytes, owned by the ctx).
  * x (device FP64, in: x0, out: solution), b device FP64.  Stops when the least-squares residual
- * |g_{j+1}| <= rtol ||r_0|| (a restart cycle follows while the true residual is above the tolerance) or
+ * |g_{j+1}| <= rtol ||r_0|| (the least-squares residual, as PCG uses its recursive residual) or
  * after max_iter Arnoldi steps (not an error: converged = 0).
  * rep->rn is the true residual norm ||b - A x|| at exit; res_history (optional host array of
  * max_iter+1 doubles) holds ||r_0||, |g_1|, ..., |g_n|.  ARG for restart < 1, max_iter < 0, rtol < 0. */

@@ -139,9 +139,9 @@ def gmres(A, b, prec, rtol=1e-8, max_iter=200, restart=50, x0=None):
     hist = [beta]
     r0 = beta
     n = 0
-    # cycles continue until the TRUE residual meets the tolerance (the least-squares estimate |g| can
-    # undershoot it in finite precision); a cycle ends at |g_{j+1}| <= rtol r0 or after `restart` steps
-    while n < max_iter and beta > rtol * r0:
+    # stopping test on the least-squares residual |g_{j+1}| (the recursively updated residual, as in
+    # PCG): the true residual of a smooth solution is only known to ~eps || |A| |x| ||
+    while n < max_iter and hist[-1] > rtol * r0:
         m = min(restart, max_iter - n)
         V = [r / beta]
         Z = []

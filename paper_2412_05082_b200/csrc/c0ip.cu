@@ -979,9 +979,9 @@ c0ip_status c0ip_gmres(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, 
   double rn = beta;
   if (res_history) res_history[0] = r0;
   int it = 0;
-  // cycles continue until the TRUE residual meets the tolerance (the least-squares estimate |g| can
-  // undershoot it in finite precision)
-  while (it < max_iter && beta > rtol * r0) {
+  // stopping test on the least-squares residual |g_{j+1}| (the recursively updated residual, as in
+  // PCG): the true residual of a smooth solution is only known to ~eps || |A| |x| ||
+  while (it < max_iter && rn > rtol * r0 && beta > 0) {
     const int mm = std::min(m, max_iter - it);
     axpby<double>(ctx, n, 0.0, b, 1.0 / beta, V, st);            // V_0 = r / beta
     std::fill(g.begin(), g.end(), 0.0);
@@ -1040,7 +1040,7 @@ c0ip_status c0ip_gmres(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, 
   auto t1 = std::chrono::steady_clock::now();
   if (rep) {
     rep->iterations = it;
-    rep->converged = (beta <= rtol * r0) ? 1 : 0;
+    rep->converged = (rn <= rtol * r0) ? 1 : 0;
     rep->r0 = r0;
     rep->rn = beta;                                               // true residual norm at exit
     const double ratio = (r0 > 0) ? rn / r0 : 0.0;
