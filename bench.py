@@ -211,6 +211,28 @@ def cpu_oracle_sample(k, seconds_target=15.0, d=2):
             "host_cpus": os.cpu_count()}
 
 
+def main_smoother(d, k, dtype):
+    """The AVS realisation bench.py times (the faster one for this d, k, dtype; see main())."""
+    return "avs_atomic" if (d == 3 or (dtype == "f64" and k == 4)) else "avs"
+
+
+def arm_config(d, k, dtype, world=1):
+    """The workload config of the timed step (shared by both arms of the bench)."""
+    N = CFG2_CELLS[k] if d == 2 else CFG4_CELLS[k]
+    n = k * N - 1
+    ndofs = n ** d
+    esz = 8 if dtype == "f64" else 4
+    sm = main_smoother(d, k, dtype)
+    kind = "atomic" if sm == "avs_atomic" else "deterministic gather"
+    return {"workload": (f"cfg2: 2D unit square, Q{k} C0IP, N={N} cells/axis ({ndofs} DoFs), one additive "
+                         f"vertex-patch smoothing step ({kind} AVS, omega=1/4)") if d == 2 else
+                        (f"cfg4: 3D unit cube, Q{k} C0IP, N={N} cells/axis ({ndofs} DoFs), one additive "
+                         f"vertex-patch smoothing step ({kind} AVS, omega=0.1)"),
+            "degree": k, "cells": N, "dofs_per_gpu": ndofs,
+            "parallelism": "replicas" if world > 1 else "single",
+            "l2": "inputs larger than L2 (x, b, r = 3 x %.0f MB)" % (ndofs * esz / 1e6)}
+
+
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -222,8 +244,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": cb["value"], "unit": "GDoF/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": (f"cfg2: 2D unit square" if d == 2 else f"cfg4: 3D unit cube") +
-                                   f" Q{k} C0IP, one AVS smoothing step (oracle-size twin)", "degree": k, "dim": d},
+            "config": arm_config(d, k, args.dtype),
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -373,7 +394,7 @@ def main():
     # AVS (residual, then every patch solve scatter-added with fire-and-forget atomics; 2D FP64
     # k = 4 on the DMMA patch kernel, 3D) or the deterministic gather AVS (2D otherwise); the other one is
     # reported beside it
-    main_sm = "avs_atomic" if (d == 3 or (args.dtype == "f64" and k == 4)) else "avs"
+    main_sm = main_smoother(d, k, args.dtype)
     other_sm = "avs" if main_sm == "avs_atomic" else "avs_atomic"
 
     def step():
@@ -498,13 +519,7 @@ def main():
         "metric": METRIC, "value": round(value, 3), "unit": "GDoF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_step_ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": (f"cfg2: 2D unit square, Q{k} C0IP, N={N} cells/axis ({ndofs} DoFs), one additive "
-                                f"vertex-patch smoothing step ({'atomic' if main_sm == 'avs_atomic' else 'deterministic gather'} AVS, omega=1/4)") if d == 2 else
-                               (f"cfg4: 3D unit cube, Q{k} C0IP, N={N} cells/axis ({ndofs} DoFs), one additive "
-                                f"vertex-patch smoothing step (atomic AVS, omega=0.1)"),
-                   "degree": k, "cells": N, "dofs_per_gpu": ndofs,
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "inputs larger than L2 (x, b, r = 3 x %.0f MB)" % (ndofs * esz / 1e6)},
+        "config": arm_config(d, k, args.dtype, world),
         "gpu_launches": int(launches),
         "clocks": clocks,
         "e2e": {"value": round(ndofs * world / (t_e2e_ms * 1e-3) / 1e9, 3), "unit": "GDoF/s",
