@@ -94,40 +94,43 @@ def flops_fdm_2d(k):
     return 2.0 * 4 * np_ ** 3 / k ** 2
 
 
+_NVML_SAMPLER = r"""
+import sys, time, pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+print("ready", mx, flush=True)
+bits = [nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+        nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap]
+t_end = time.time() + float(sys.argv[2])
+while time.time() < t_end:
+    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+    rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+    print(sm, *[int(bool(rs & b)) for b in bits], flush=True)
+    time.sleep(0.002)
+"""
+
+
 class ClockSampler:
-    """SM clock and clock-event (throttle) reasons sampled DURING the timed region: NVML every ~1 ms
-    from a thread (nvidia_ml_py), falling back to nvidia-smi every 0.2 s."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region by a separate
+    process polling NVML every ~2 ms (no GIL contention with the launching thread); nvidia-smi
+    fallback every 0.2 s."""
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device_index):
+    def __init__(self, device_index, max_seconds=120.0):
         self.idx = device_index
+        self.max_seconds = max_seconds
         self.samples = []           # (sm_mhz, max_mhz, set of reason names)
         self.source = "nvml"
+        self.proc = None
+        self.mx = 0.0
         self._stop = threading.Event()
         self._t = None
 
-    def _run_nvml(self):
-        import pynvml as nv
-        nv.nvmlInit()
-        try:
-            h = nv.nvmlDeviceGetHandleByIndex(self.idx)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            bits = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
-                    "hw_thermal_slowdown": nv.nvmlClocksThrottleReasonHwThermalSlowdown,
-                    "sw_thermal_slowdown": nv.nvmlClocksThrottleReasonSwThermalSlowdown,
-                    "sw_power_cap": nv.nvmlClocksThrottleReasonSwPowerCap}
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.samples.append((float(sm), float(mx), {k for k, v in bits.items() if rs & v}))
-                self._stop.wait(0.001)
-        finally:
-            nv.nvmlShutdown()
-
     def _run_smi(self):
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
@@ -137,27 +140,43 @@ class ClockSampler:
                     f = [x.strip() for x in out.split(",")]
                     if f[1].replace(".", "").isdigit():
                         self.samples.append((float(f[1]), float(f[2]) if f[2].replace(".", "").isdigit() else 0.0,
-                                             {n for n, v in zip(names, f[5:9]) if v.lower() == "active"}))
+                                             {n for n, v in zip(self.NAMES, f[5:9]) if v.lower() == "active"}))
             except Exception:
                 pass
             self._stop.wait(0.2)
 
-    def _run(self):
-        try:
-            self._run_nvml()
-        except Exception:
-            self.source = "nvidia-smi"
-            self._run_smi()
-
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
-        time.sleep(0.01)            # first sample before the timed region starts
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", _NVML_SAMPLER, str(self.idx), str(self.max_seconds)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline().split()
+            if not first or first[0] != "ready":
+                raise RuntimeError("nvml sampler did not start")
+            self.mx = float(first[1])
+        except Exception:
+            if self.proc:
+                self.proc.kill()
+            self.proc = None
+            self.source = "nvidia-smi"
+            self._t = threading.Thread(target=self._run_smi, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=10)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            for line in out.splitlines():
+                f = line.split()
+                if len(f) == 5 and f[0].isdigit():
+                    self.samples.append((float(f[0]), self.mx, {n for n, v in zip(self.NAMES, f[1:]) if v == "1"}))
+        else:
+            self._stop.set()
+            self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
