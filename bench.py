@@ -650,13 +650,13 @@ def main():
             rg = {}
             for name, cdt in (("fp64", torch.float64), ("mixed", torch.float32)):
                 mg = api.MG("mvs", 1, om_m, symmetric=False, cycle_dtype=cdt)
-                cm.gmres(mg, bm, max_iter=2)
+                cm.gmres(mg, bm, max_iter=2, restart=30)      # warm-up: workspace, V-cycle graph
                 torch.cuda.synchronize()
-                xs, rep, hist = cm.gmres(mg, bm, max_iter=60, restart=60)
+                xs, rep, hist = cm.gmres(mg, bm, max_iter=60, restart=30)
                 rg[name] = {"seconds": round(rep["seconds"], 4), "iterations": rep["iterations"],
                             "nu": round(rep["nu"], 2), "converged": rep["converged"]}
             rg["dofs"] = rm["dofs"]
-            rg["config"] = rm["config"].replace("CG", "FGMRES(60)").replace("reversed order in post-smoothing",
+            rg["config"] = rm["config"].replace("CG", "FGMRES(30)").replace("reversed order in post-smoothing",
                                                                           "same order in post-smoothing")
             rg["mixed_speedup"] = round(rg["fp64"]["seconds"] / rg["mixed"]["seconds"], 3)
             line["gmres_mvs"] = rg

@@ -955,7 +955,8 @@ c0ip_status c0ip_gmres(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, 
   auto t0 = std::chrono::steady_clock::now();
   Level& L = ctx->levels[ctx->lmax];
   const int64_t n = L.ndofs;
-  const int m = std::max(1, std::min<int>(restart, std::max(1, max_iter)));
+  const int m = restart;          // workspace sized by restart (reused across calls: no allocation
+                                  // inside a timed solve after the first call with this restart)
   // Flexible right-preconditioned GMRES(m) (Saad Alg. 9.6), modified Gram-Schmidt, Givens rotations
   // (GMRES outer solver for the multiplicative smoother)
   ctx->gm_V.alloc(n * (m + 1));
