@@ -306,7 +306,7 @@ __device__ double op1d(const Coef2<double, K>& c, int which, int64_t jo, int64_t
 }
 
 template <int K>
-__global__ void __launch_bounds__(256, 3) mvs2d_mma_kernel(const __grid_constant__ MvsP<double, K> P) {
+__global__ void __launch_bounds__(256, 4) mvs2d_mma_kernel(const __grid_constant__ MvsP<double, K> P) {
   using MV = MvsMma<K>;
   constexpr int NP = MV::NP, CML = MV::CML, CB = MV::CB, NY = MV::NY, NX = MV::NX;
   constexpr int NT = 256;
