@@ -488,7 +488,7 @@ __device__ __forceinline__ void sdot_var(const Coef2<T, K>& c, int var, const T 
 // registers.  r lines are read from global memory, the x update is a read-modify-write (disjoint
 // patch list) or red.global.add (atomic AVS) restricted to the owned node planes.
 template <typename T, int K>
-__global__ void __launch_bounds__(256, 3) patch_fdm3d_kernel(const __grid_constant__ Fdm3P<T, K> P) {
+__global__ void __launch_bounds__(256, (K == 3 && sizeof(T) == 8) ? 3 : 4) patch_fdm3d_kernel(const __grid_constant__ Fdm3P<T, K> P) {
   using LY = Fdm3Layout<T, K>;
   constexpr int NP = LY::NP, NL2 = LY::NL2, LPL = LY::LPL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
