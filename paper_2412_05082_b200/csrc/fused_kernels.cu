@@ -45,6 +45,25 @@ __host__ __device__ constexpr int pick_rb(int lines, int mult, int maxrb) {
   return best;
 }
 
+// acc[r] += c * w[r][o] over the RB lines of a thread; FP32 pairs go through the packed FFMA2 (f32x2
+// FMA with a scalar uniform operand on sm_100a: two FMAs per issue slot)
+template <typename T, int RB, int W>
+__device__ __forceinline__ void fma_rb(T c, const T (&w)[RB][W], int o, T (&acc)[RB]) {
+  if constexpr (std::is_same<T, float>::value && RB >= 2) {
+#pragma unroll
+    for (int r = 0; r + 1 < RB; r += 2) {
+      const float2 v = __ffma2_rn(make_float2(c, c), make_float2(w[r][o], w[r + 1][o]),
+                                  make_float2(acc[r], acc[r + 1]));
+      acc[r] = v.x;
+      acc[r + 1] = v.y;
+    }
+    if constexpr (RB % 2 == 1) acc[RB - 1] = fmaf(c, w[RB - 1][o], acc[RB - 1]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[r] = fma(c, w[r][o], acc[r]);
+  }
+}
+
 // Interior rows of all K classes of one cell at once, window index outermost so that every DFMA
 // of an accumulator is separated by the other 3K*RB (or K*RB) accumulators (ILP), coefficients
 // shared by the RB lines.  w[r][o] <-> node (c-2)K + o.
@@ -61,18 +80,12 @@ __device__ __forceinline__ void x_all_interior(const Coef2<T, K>& c, const T (&w
     for (int p = 0; p < K; ++p) {
       const int q = o - p;                           // B coefficient index (offset q - 2K)
       if (q >= 0 && q <= 4 * K && (p == 0 || (q >= K - p && q <= 4 * K - p))) {
-        const T cb = c.BI[p][q];
-#pragma unroll
-        for (int r = 0; r < RB; ++r) ob[p][r] = fma(cb, w[r][o], ob[p][r]);
+        fma_rb<T, RB>(c.BI[p][q], w, o, ob[p]);
       }
       const int qm = o - p - K;                      // M/L coefficient index (offset qm - K)
       if (qm >= 0 && qm <= 2 * K && (p == 0 || (qm >= K - p && qm <= 2 * K - p))) {
-        const T cl = c.LI[p][qm], cm = c.MI[p][qm];
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-          ol[p][r] = fma(cl, w[r][o], ol[p][r]);
-          om[p][r] = fma(cm, w[r][o], om[p][r]);
-        }
+        fma_rb<T, RB>(c.LI[p][qm], w, o, ol[p]);
+        fma_rb<T, RB>(c.MI[p][qm], w, o, om[p]);
       }
     }
 }
@@ -89,9 +102,7 @@ __device__ __forceinline__ void y_all_interior(const Coef2<T, K>& c, const T (&w
       const bool ok = (WHICH == 0) ? (q >= 0 && q <= 4 * K && (p == 0 || (q >= K - p && q <= 4 * K - p)))
                                    : (q >= 0 && q <= 2 * K && (p == 0 || (q >= K - p && q <= 2 * K - p)));
       if (ok) {
-        const T cq = (WHICH == 0) ? c.BI[p][q] : (WHICH == 1 ? c.MI[p][q] : c.LI[p][q]);
-#pragma unroll
-        for (int r = 0; r < RB; ++r) acc[p][r] = fma(cq, w[r][o], acc[p][r]);
+        fma_rb<T, RB>((WHICH == 0) ? c.BI[p][q] : (WHICH == 1 ? c.MI[p][q] : c.LI[p][q]), w, o, acc[p]);
       }
     }
 }
@@ -106,11 +117,12 @@ struct ApplyLayout {
   static constexpr int XN = O * PX;                // the O new box rows of a tile below the previous one
   static constexpr int STAGE = BW * PO;            // one of the three x-stage outputs
   static constexpr int TOTAL = XB + 2 * XN + 2 * BB + 3 * STAGE;
-  // register blocking: the column-walk stages have few units (O rows x C cells); for k = 4 blocking RB
-  // lines per thread (one LDCU per RB DFMA, half the threads idle) measured faster than the balanced
-  // choice of pick_rb, for the other degrees slower (0.205 -> 0.196 ms at k = 4; k = 2, 5 regress)
-  static constexpr int RBX = pick_rb(BW, C, RB), RBY = (K == 4) ? RB : pick_rb(O, C, RB);
-  static constexpr int RBXN = (K == 4) ? RB : pick_rb(O, C, RB);   // x-stage on the O new rows only
+  // register blocking: the column-walk stages have few units (O rows x C cells); for FP64 k = 4 blocking
+  // RB lines per thread (one LDCU per RB DFMA, half the threads idle) measured faster than the balanced
+  // choice of pick_rb, for the other degrees and FP32 slower (0.205 -> 0.196 ms at k = 4)
+  static constexpr bool FORCE = (K == 4 && sizeof(T) == 8);
+  static constexpr int RBX = pick_rb(BW, C, RB), RBY = FORCE ? RB : pick_rb(O, C, RB);
+  static constexpr int RBXN = FORCE ? RB : pick_rb(O, C, RB);   // x-stage on the O new rows only
   static_assert(BW - O <= O, "carried rows must not overlap the rows they are copied from");
   static constexpr int GX = cdiv(BW, RBX);         // row groups of the x-stage
   static constexpr int GY = cdiv(O, RBY);          // column groups of the y-stage
