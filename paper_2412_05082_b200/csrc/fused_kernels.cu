@@ -406,8 +406,19 @@ __device__ __forceinline__ void s_t(const Coef2<T, K>& c, const T (&w)[RB][2 * K
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
       const T s = c.S[V][l * NP + i];
+      if constexpr (std::is_same<T, float>::value && RB >= 2) {
 #pragma unroll
-      for (int r = 0; r < RB; ++r) z[r][i] = fma(s, w[r][l], z[r][i]);
+        for (int r = 0; r + 1 < RB; r += 2) {
+          const float2 v = __ffma2_rn(make_float2(s, s), make_float2(w[r][l], w[r + 1][l]),
+                                      make_float2(z[r][i], z[r + 1][i]));
+          z[r][i] = v.x;
+          z[r + 1][i] = v.y;
+        }
+        if constexpr (RB % 2 == 1) z[RB - 1][i] = fmaf(s, w[RB - 1][l], z[RB - 1][i]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RB; ++r) z[r][i] = fma(s, w[r][l], z[r][i]);
+      }
     }
 }
 
@@ -420,8 +431,19 @@ __device__ __forceinline__ void s_rows(const Coef2<T, K>& c, const T (&z)[RB][2 
 #pragma unroll
     for (int p = P0; p < K; ++p) {
       const T s = c.S[V][(OFF + p) * NP + i];
+      if constexpr (std::is_same<T, float>::value && RB >= 2) {
 #pragma unroll
-      for (int r = 0; r < RB; ++r) out[r][p] = fma(s, z[r][i], out[r][p]);
+        for (int r = 0; r + 1 < RB; r += 2) {
+          const float2 v = __ffma2_rn(make_float2(s, s), make_float2(z[r][i], z[r + 1][i]),
+                                      make_float2(out[r][p], out[r + 1][p]));
+          out[r][p] = v.x;
+          out[r + 1][p] = v.y;
+        }
+        if constexpr (RB % 2 == 1) out[RB - 1][p] = fmaf(s, z[RB - 1][i], out[RB - 1][p]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < RB; ++r) out[r][p] = fma(s, z[r][i], out[r][p]);
+      }
     }
 }
 
