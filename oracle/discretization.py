@@ -13,7 +13,10 @@ ev, eh (PAPER.md:268-312):
 with a = [phi'] the jump of the derivative (sum of outward normal derivatives,
 PAPER.md:87-97) and b = {phi''} the mean of the second derivative; on the two boundary
 facets the one-sided definitions of PAPER.md:100-106 (reading Q26): a = d_n phi,
-b = d_n^2 phi.  h_f = harmonic mean of the adjacent cell widths, i.e. h.
+b = d_n^2 phi.  h_f = harmonic mean of the adjacent cell widths, i.e. h on an
+interior facet.  On a boundary facet the harmonic-mean rule names a single cell; reading Q27
+ takes h_f = h/2 there, i.e. the boundary (Nitsche) penalty is BOUNDARY_PENALTY x
+the interior one (the variant that reproduces PAPER.md Tables 1-2).
 sigma is an input (reading Q4: default k(k+1)).  Rows/columns of nodes 0 and kN are
 eliminated (u = 0 strongly, reading Q26).
 """
@@ -21,6 +24,9 @@ import numpy as np
 import scipy.sparse as sp
 
 from .basis import Basis1D, gauss_legendre
+
+
+BOUNDARY_PENALTY = 2.0   # reading Q27: sigma/h_f on boundary facets with h_f = h/2
 
 
 def default_sigma(k, penalty_scale=1.0):
@@ -66,8 +72,10 @@ def face_vectors_1d(k, h):
     }
 
 
-def global_matrices_1d(k, N, sigma, eliminate=True, nq=None):
-    """Global 1D M, L, B (scipy CSR).  Size (kN+1)^2, or (kN-1)^2 after elimination."""
+def global_matrices_1d(k, N, sigma, eliminate=True, nq=None, bfac=BOUNDARY_PENALTY):
+    """Global 1D M, L, B (scipy CSR).  Size (kN+1)^2, or (kN-1)^2 after elimination.
+
+    bfac: boundary-facet penalty factor (reading Q27; bfac=1 is SURVEY.md Appendix A)."""
     h = 1.0 / N
     Mc, Lc, Bc = element_matrices_1d(k, h, nq)
     fv = face_vectors_1d(k, h)
@@ -81,13 +89,14 @@ def global_matrices_1d(k, N, sigma, eliminate=True, nq=None):
         vm.append(Mc.ravel()); vl.append(Lc.ravel()); vb.append(Bc.ravel())
     zeros = lambda n: np.zeros(n)
     for f in range(N + 1):
+        s_f = sigma
         if f == 0:
-            a, b = fv["lower"]; g = loc
+            a, b = fv["lower"]; g = loc; s_f = bfac * sigma
         elif f == N:
-            a, b = fv["upper"]; g = (N - 1) * k + loc
+            a, b = fv["upper"]; g = (N - 1) * k + loc; s_f = bfac * sigma
         else:
             a, b = fv["interior"]; g = (f - 1) * k + np.arange(2 * k + 1)
-        F = (sigma / h) * np.outer(a, a) - np.outer(a, b) - np.outer(b, a)
+        F = (s_f / h) * np.outer(a, a) - np.outer(a, b) - np.outer(b, a)
         rr, cc = np.meshgrid(g, g, indexing="ij")
         rows.append(rr.ravel()); cols.append(cc.ravel())
         vm.append(zeros(F.size)); vl.append(zeros(F.size)); vb.append(F.ravel())

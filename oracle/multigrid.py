@@ -26,6 +26,17 @@ from .smoothers import PatchSolvers, smooth
 from .mesh import level_cells
 
 
+def default_omega(d, kind, exact=False):
+    """Damping of the experiments: AVS 1/4 in 2D (PAPER.md:213, 528), 0.1 in 3D (PAPER.md:617);
+    MVS 1 with exact local solvers, 0.7 in 3D and, where the paper
+    gives no value (2D, inexact local solvers), 0.8 (reading Q28)."""
+    if kind == "avs":
+        return 0.25 if d == 2 else 0.1
+    if exact:
+        return 1.0
+    return 0.8 if d == 2 else 0.7
+
+
 def embedding_1d(k, Nc):
     """E (n_f x n_c): coarse global basis (Nc cells) evaluated at the fine (2Nc) interior nodes."""
     Nf = 2 * Nc
@@ -77,8 +88,8 @@ class Hierarchy:
         for ps in self.ps.values():
             if not hasattr(ps, "groups64"):
                 ps.groups64 = ps.groups
-            ps.groups = {key: (ids, (fac[0].astype(dtype), fac[1]), At.astype(dtype))
-                         for key, (ids, fac, At) in ps.groups64.items()}
+            ps.groups = {key: (ids, Ainv.astype(dtype), At.astype(dtype))
+                         for key, (ids, Ainv, At) in ps.groups64.items()}
 
 
 def vcycle(h, l, x, b, kind, steps, omega, symmetric=True):
@@ -191,3 +202,28 @@ def fractional_iterations(hist):
     if ratio == 0.0:
         return 0.0
     return -8.0 / np.log10(ratio ** (1.0 / n))
+
+
+def solve_paper(d, k, L, kind, steps, exact=False, omega=None, cycle_dtype=np.float64, rtol=1e-8):
+    """One solve of the paper's experiment protocol: x0 = 0, F =
+    operator.paper_rhs (reading Q8b), boundary penalty per reading Q27.  AVS: CG with the symmetric
+    cycle; MVS: GMRES (FGMRES(50)) with the same-order cycle (reading Q11).  `steps` pre- and
+    post-smoothing steps, omega = default_omega unless given; exact=True uses A_v = R_v A R_v^T
+    (Table 1).  Returns (iterations, nu, Hierarchy)."""
+    from .operator import paper_rhs
+    from .smoothers import PatchSolvers
+    from .discretization import default_sigma
+    s = default_sigma(k)
+    h = Hierarchy(k, d, L, s)
+    if exact:
+        for l in h.A:
+            h.ps[l] = PatchSolvers(k, d, level_cells(l), s, exact_A=h.A[l])
+    h.set_dtype(cycle_dtype)
+    om = default_omega(d, kind, exact) if omega is None else omega
+    b = paper_rhs(k, d, level_cells(L), s)
+    if kind == "avs":
+        _, n, hist = pcg(h.A[L], b, lambda r: precondition(h, r, kind, steps, om), rtol=rtol)
+    else:
+        _, n, hist = gmres(h.A[L], b, lambda r: precondition(h, r, kind, steps, om, symmetric=False),
+                           rtol=rtol, restart=50)
+    return n, fractional_iterations(hist), h

@@ -7,8 +7,9 @@ contraction  int_K grad^2 u : grad^2 v  (including the mixed 2 d_xy u d_xy v ter
 PAPER.md:53, 119) plus, on every facet, the penalty, consistency and adjoint
 consistency terms  (sigma/h_e)[d_n u][d_n v] - {d_n^2 u}[d_n v] - [d_n u]{d_n^2 v}
  with the jump/mean of PAPER.md:87-106 (one-sided on boundary
-facets, reading Q26).  It does NOT use the Kronecker form of PAPER.md:314-342; the
-Kronecker identity is a test that compares the two.
+facets, reading Q26) and h_e = h on interior, h/2 on boundary facets (reading Q27).  It does
+NOT use the Kronecker form of PAPER.md:314-342; the Kronecker identity is a
+test that compares the two.
 
 Numbering: full nodes j_a = 0..kN per axis, interior index
 i_a = j_a - 1, global id sum_a i_a n^a with n = kN-1 (x fastest).
@@ -18,6 +19,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from .basis import Basis1D, gauss_legendre
+from .discretization import BOUNDARY_PENALTY
 
 
 def _tensor(tables):
@@ -49,11 +51,12 @@ def reference_cell_matrix(k, d, h, nq=None):
     return K
 
 
-def reference_face_matrix(k, d, h, axis, kind, sigma, nq=None):
+def reference_face_matrix(k, d, h, axis, kind, sigma, nq=None, bfac=BOUNDARY_PENALTY):
     """Face matrix for a facet perpendicular to `axis`.
 
     kind='interior': (2 nl)^2 on [dofs of lower cell K^- | dofs of upper cell K^+].
-    kind='lower'/'upper': nl^2 on the one cell touching the boundary facet x_axis=0 / =1.
+    kind='lower'/'upper': nl^2 on the one cell touching the boundary facet x_axis=0 / =1;
+    penalty sigma/h_e with h_e = h/bfac there (reading Q27).
     """
     bas = Basis1D(k)
     nq = nq or (k + 2)
@@ -75,8 +78,10 @@ def reference_face_matrix(k, d, h, axis, kind, sigma, nq=None):
         J = np.vstack([Jm, Jp]); Mn = np.vstack([Mm, Mp])
     elif kind == "lower":
         J, Mn = -trace(0.0, 1), trace(0.0, 2)
+        sigma = bfac * sigma
     elif kind == "upper":
         J, Mn = trace(1.0, 1), trace(1.0, 2)
+        sigma = bfac * sigma
     else:
         raise ValueError(kind)
     JW, MW = J * Wf, Mn * Wf
@@ -92,7 +97,7 @@ def _local_full_ids(k, d, N, cells):
     return (j * strides).sum(-1)
 
 
-def assemble_full(k, d, N, sigma, cells=None):
+def assemble_full(k, d, N, sigma, cells=None, bfac=BOUNDARY_PENALTY):
     """COO->CSR of the C0IP form over full nodes (boundary nodes included).
 
     cells: optional [m, d] int array of included cells (a window); all faces whose adjacent
@@ -117,8 +122,8 @@ def assemble_full(k, d, N, sigma, cells=None):
     add(ids, Kc)
     for a in range(d):
         Fi = reference_face_matrix(k, d, h, a, "interior", sigma)
-        Fl = reference_face_matrix(k, d, h, a, "lower", sigma)
-        Fu = reference_face_matrix(k, d, h, a, "upper", sigma)
+        Fl = reference_face_matrix(k, d, h, a, "lower", sigma, bfac=bfac)
+        Fu = reference_face_matrix(k, d, h, a, "upper", sigma, bfac=bfac)
         lo = cells[cells[:, a] == 0]
         if len(lo):
             add(_local_full_ids(k, d, N, lo), Fl)
@@ -148,9 +153,9 @@ def interior_full_ids(k, d, N):
     return idx.ravel()
 
 
-def assemble(k, d, N, sigma):
+def assemble(k, d, N, sigma, bfac=BOUNDARY_PENALTY):
     """A_ell over interior DoFs (CSR), boundary rows/cols eliminated (reading Q26)."""
-    Af = assemble_full(k, d, N, sigma)
+    Af = assemble_full(k, d, N, sigma, bfac=bfac)
     keep = interior_full_ids(k, d, N)
     return Af[keep][:, keep].tocsr()
 
@@ -185,6 +190,62 @@ def paper_load(d):
             out = out * np.sin(np.pi * x)
         return out
     return f
+
+
+def paper_solution(d):
+    """u*(x) = prod_a sin(pi x_a), the analytical solution of the experiments."""
+    def u(*xs):
+        out = 1.0
+        for x in xs:
+            out = out * np.sin(np.pi * x)
+        return out
+    return u
+
+
+def boundary_data_load(k, d, N, sigma, nq=None, bfac=BOUNDARY_PENALTY):
+    """Nitsche boundary-data part of F for d_n u = g on the boundary (reading Q8b).
+
+    PAPER.md:488 fixes u* = prod sin(pi x_a) as the solution; u* = 0 on the boundary but its
+    normal derivative g = d_n u* is not zero, so the clamped condition d_n u = g is imposed weakly
+    by the terms that the boundary facets of Eq. bfc0ip (one-sided jump/mean
+    PAPER.md:100-106) generate with [d_n u] -> d_n u - g:
+        F_bd(v) = sum_{e in F^bd} int_e g ( (sigma/h_e) d_n v - d_n^2 v ) ds,
+    with h_e = h/bfac (reading Q27).  On the facet x_a = 0 (outward normal -e_a) and x_a = 1
+    (normal +e_a): g = d_n u* = -pi prod_{b != a} sin(pi x_b).  Facet quadrature: k+3 Gauss points
+    per cell and tangential axis.
+    """
+    h = 1.0 / N
+    nq = nq or (k + 3)
+    bas = Basis1D(k)
+    t, w = gauss_legendre(nq)
+    V = bas.eval(t, 0)
+    Wf = _tensor([w[None, :]] * (d - 1)).ravel() * h ** (d - 1) if d > 1 else np.ones(1)
+    tq = np.array(list(itertools.product(range(nq), repeat=d - 1)))[:, ::-1] if d > 1 else np.zeros((1, 0), int)
+    nn = k * N + 1
+    bf = np.zeros(nn ** d)
+    for a in range(d):
+        for side in (0, 1):
+            tn = float(side)
+            sgn = 1.0 if side == 1 else -1.0
+            # traces on the facet: [nl, Qf] for d_n phi and d_n^2 phi (x fastest over the cell's dofs)
+            tabs1 = [V] * d; tabs1[a] = sgn * bas.eval(tn, 1) / h
+            tabs2 = [V] * d; tabs2[a] = bas.eval(tn, 2) / h ** 2
+            Dn1, Dn2 = _tensor(tabs1), _tensor(tabs2)
+            cells = np.array(list(itertools.product(range(N), repeat=d)))[:, ::-1]
+            cells = cells[cells[:, a] == (0 if side == 0 else N - 1)]
+            others = [b for b in range(d) if b != a]
+            g = -np.pi * np.ones((len(cells), len(Wf)))
+            for j, b in enumerate(others):
+                g = g * np.sin(np.pi * (cells[:, b][:, None] + t[tq[:, j]][None, :]) * h)
+            contrib = (g * Wf) @ ((bfac * sigma / h) * Dn1 - Dn2).T        # [ncells, nl]
+            np.add.at(bf, _local_full_ids(k, d, N, cells).ravel(), contrib.ravel())
+    return bf[interior_full_ids(k, d, N)]
+
+
+def paper_rhs(k, d, N, sigma, bfac=BOUNDARY_PENALTY):
+    """F of the solve experiments: int f v with f = Delta^2 u* plus the
+    boundary-data terms of boundary_data_load, so that u_h -> u* = prod sin(pi x_a)."""
+    return rhs_load(k, d, N, paper_load(d)) + boundary_data_load(k, d, N, sigma, bfac=bfac)
 
 
 def dof_coords(k, N, i):

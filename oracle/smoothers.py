@@ -8,8 +8,9 @@ coloured MVS: for each colour c in order,
 (sign "+" per reading Q2).  A~_v is the separable surrogate of Eq. localsolverbila
 (PAPER.md:369-384): A~_v = sum_a B_{v,a} (x) (x)_{b!=a} M_{v,b}, built from principal
 submatrices of the 1D matrices in numpy.kron order (z,y,x; x fastest,
-reading Q17).  The oracle inverts A~_v densely by Cholesky with one step of iterative
-refinement -- never by fast diagonalisation.  The exact local solver
+reading Q17).  The oracle inverts A~_v densely (Cholesky solve against the identity, refined once)
+-- never by fast diagonalisation -- and applies the explicit inverse to all patches of a variant
+tuple as one matrix product followed by one step of iterative refinement.  The exact local solver
 A_v = R_v A R_v^T (Table 1) is available for tests.
 """
 import numpy as np
@@ -49,20 +50,24 @@ class PatchSolvers:
             else:
                 g = self.dofs[ids[0]]
                 At = exact_A[np.ix_(g, g)].toarray() if hasattr(exact_A, "toarray") else exact_A[np.ix_(g, g)]
-            self.groups[key] = (ids, sla.cho_factor(At), At)
+            fac = sla.cho_factor(At)
+            eye = np.eye(At.shape[0])
+            Ainv = sla.cho_solve(fac, eye)
+            Ainv = Ainv + sla.cho_solve(fac, eye - At @ Ainv)      # one refinement step
+            self.groups[key] = (ids, 0.5 * (Ainv + Ainv.T), At)
         self.exact = exact_A is not None
 
     def solve(self, ids, R):
-        """U[i] = A~_{v_i}^{-1} R[i] for patches ids (rows of R), with one refinement step."""
+        """U[i] = A~_{v_i}^{-1} R[i] for patches ids (rows of R): U = R A~^{-1} (A~ symmetric), then one
+        step of iterative refinement U += (R - U A~) A~^{-1}."""
         out = np.empty_like(R)
-        for key, (gids, fac, At) in self.groups.items():
+        for key, (gids, Ainv, At) in self.groups.items():
             mask = np.isin(ids, gids)
             if not mask.any():
                 continue
-            rhs = R[mask].T
-            u = sla.cho_solve(fac, rhs)
-            u = u + sla.cho_solve(fac, rhs - At @ u)
-            out[mask] = u.T
+            Rg = R[mask]
+            U = Rg @ Ainv
+            out[mask] = U + (Rg - U @ At) @ Ainv
         return out
 
 
@@ -138,7 +143,7 @@ def avs_delta_sample(k, d, N, sigma, x, b, omega, sample):
                                      for bb in range(d)])
             fac = sla.cho_factor(At)
             u = sla.cho_solve(fac, rv)
-            u = u + sla.cho_solve(fac, rv - At @ u)
+            u = u + sla.cho_solve(fac, rv - At @ u)      # one refinement step
             loc = int(np.nonzero(pd == g)[0][0])
             out[s] += omega * u[loc]
     return out

@@ -32,8 +32,9 @@ def test_gauss_rule_exactness(nq):
         assert abs((w * t ** p).sum() - 1.0 / (p + 1)) < 1e-14
 
 
-def _exact_1d(k, N, sigma):
-    """Independent exact construction with sympy (symbolic integration, GL nodes in radicals)."""
+def _exact_1d(k, N, sigma, bfac=2):
+    """Independent exact construction with sympy (symbolic integration, GL nodes in radicals).
+    bfac: boundary-facet penalty factor (reading Q27: 2; 1)."""
     t = sy.symbols("t")
     nodes = [sy.Integer(0)] + sorted(sy.solve(sy.diff(sy.legendre(k, 2 * t - 1), t), t),
                                      key=lambda e: float(e)) + [sy.Integer(1)]
@@ -68,20 +69,31 @@ def _exact_1d(k, N, sigma):
                 g = f * k + m
                 a[g] = a.get(g, 0) - d1(m, 0)
                 b[g] = b.get(g, 0) + (d2(m, 0) if f == 0 else d2(m, 0) / 2)
+        sf = sigma * (bfac if f in (0, N) else 1)
         for i in a:
             for j in a:
-                Bf[i, j] += sigma / h * a[i] * a[j] - a[i] * b[j] - b[i] * a[j]
+                Bf[i, j] += sf / h * a[i] * a[j] - a[i] * b[j] - b[i] * a[j]
     sl = slice(1, nn - 1)
     return [np.array(X[sl, sl].evalf(30).tolist(), dtype=float) for X in (Mf, Lf, Bf)]
 
 
 def test_golden_k2_N2_appendix_A():
+    """SURVEY.md Appendix A (boundary penalty = interior penalty, bfac=1)."""
     g = read_matrices("k2_N2_sigma6_1d.txt")
-    M, L, B = (X.toarray() for X in global_matrices_1d(2, 2, 6.0))
+    M, L, B = (X.toarray() for X in global_matrices_1d(2, 2, 6.0, bfac=1.0))
     assert np.allclose(M, g["M"], rtol=0, atol=1e-13)
     assert np.allclose(L, g["L"], rtol=0, atol=1e-12)
     assert np.allclose(B, g["B"], rtol=1e-14, atol=1e-10)
     assert np.allclose(np.linalg.eigvalsh(B), [137.2648, 768.0, 3222.7352], atol=1e-4)
+
+
+def test_golden_k2_N2_boundary_penalty_2():
+    """tests/golden/k2_N2_sigma6_bfac2_1d.txt (exact rationals by tests/golden/make_bfac2.py, sympy
+    only): reading Q27 adds (sigma/h) a a^T once more on each boundary facet."""
+    g = read_matrices("k2_N2_sigma6_bfac2_1d.txt")
+    M, L, B = (X.toarray() for X in global_matrices_1d(2, 2, 6.0))
+    assert np.allclose(M, g["M"], rtol=0, atol=1e-13)
+    assert np.allclose(B, g["B"], rtol=1e-14, atol=1e-10)
 
 
 def test_cell_mass_spec_example():

@@ -5,7 +5,7 @@ import scipy.sparse.linalg as spla
 
 from oracle.multigrid import (embedding_1d, prolongation, Hierarchy, vcycle, precondition, pcg,
                               fractional_iterations)
-from oracle.operator import dof_coords, rhs_load, paper_load
+from oracle.operator import dof_coords, rhs_load, paper_load, paper_rhs
 from oracle.mesh import level_cells
 from oracle.discretization import default_sigma
 from c0ip_inputs import uniform
@@ -75,7 +75,7 @@ def test_cfg1_pcg_matches_direct(h2):
     """cfg1 (2D, Q2, 8x8): MG-PCG to 1e-8 equals the dense direct solve."""
     L = 3
     A = h2.A[L]
-    b = rhs_load(2, 2, level_cells(L), paper_load(2))
+    b = paper_rhs(2, 2, level_cells(L), default_sigma(2))
     x, n, hist = pcg(A, b, lambda r: precondition(h2, r, "avs", 2, 0.25))
     xd = spla.spsolve(A.tocsc(), b)
     assert hist[-1] <= 1e-8 * hist[0]
@@ -85,17 +85,15 @@ def test_cfg1_pcg_matches_direct(h2):
 
 @pytest.mark.parametrize("k", [2, 3, 4])
 def test_mixed_precision_iterations(k):
-    """PAPER.md:747 / SPEC.md:490: FP32 cycle in FP64 CG -> same accuracy, iteration count close.
-
-    The oracle's FP32 cycle rounds the dense Cholesky factors (reading Q21); with plain
-    (non-flexible) CG this costs up to 2 iterations here."""
-    L = 4
+    """PAPER.md:747 (goddeke2007: FP32 V-cycle inside FP64 CG reaches the FP64 accuracy with the same
+    iteration count): the oracle's FP32 cycle (every table rounded, reading Q21) within 1 iteration."""
+    L = 5
     h = Hierarchy(k, 2, L, default_sigma(k))
-    b = rhs_load(k, 2, level_cells(L), paper_load(2))
+    b = paper_rhs(k, 2, level_cells(L), default_sigma(k))
     _, n64, _ = pcg(h.A[L], b, lambda r: precondition(h, r, "avs", 2, 0.25))
     h.set_dtype(np.float32)
     x32, n32, hist = pcg(h.A[L], b, lambda r: precondition(h, r, "avs", 2, 0.25))
-    assert abs(n32 - n64) <= 2
+    assert abs(n32 - n64) <= 1, (n32, n64)
     assert np.linalg.norm(b - h.A[L] @ x32) <= 1.01e-8 * np.linalg.norm(b)
 
 
@@ -114,7 +112,7 @@ def test_two_grid_h_independent():
             x = smooth(A, h.ps[L], np.zeros_like(r), r, "avs", 2, 0.25)
             x = x + P @ lu.solve(P.T @ (r - A @ x))
             return smooth(A, h.ps[L], x, r, "avs", 2, 0.25)
-        b = rhs_load(k, 2, level_cells(L), paper_load(2))
+        b = paper_rhs(k, 2, level_cells(L), default_sigma(k))
         nus.append(fractional_iterations(pcg(A, b, tg)[2]))
     assert abs(nus[1] - nus[0]) < 1.5 and nus[1] < 20
 
@@ -173,3 +171,48 @@ def test_gmres_with_nonsymmetric_mvs_cycle_solves_cfg1():
     xd = np.linalg.solve(A.toarray(), b)
     assert np.linalg.norm(x - xd) <= 1e-8 * np.linalg.norm(xd)
     assert it <= 15
+
+
+# ------------------------------------------------------------------------------ the paper's iteration counts
+# (d, k, L, smoother, steps, exact) -> (paper nu, allowed deviation).  PAPER.md Table 1 (exact local
+# solvers) and Table 2 (FDM surrogate); the protocol and the
+# readings (Q8b boundary data, Q27 boundary penalty, Q28 MVS damping) are DESIGN.md §2 / §2b.
+PAPER_GATES = {
+    "table2_avs2_k2_L7": ((2, 2, 7, "avs", 2, False), 19.2, 2.0),
+    "table2_avs2_k4_L6": ((2, 4, 6, "avs", 2, False), 9.2, 1.0),
+    "table2_mvs1_k4_L6": ((2, 4, 6, "mvs", 1, False), 4.2, 1.0),
+    "table1_avs2_k4_L6": ((2, 4, 6, "avs", 2, True), 10.3, 1.0),
+    "table1_mvs1_k4_L6": ((2, 4, 6, "mvs", 1, True), 2.9, 1.0),
+    "table2_avs2_k4_L5": ((2, 4, 5, "avs", 2, False), None, None),   # level-uniformity partner
+    # Table 3 (3D): the paper's 3D level L has 2^(L-1) cells per axis (reading Q9b),
+    # i.e. the oracle's level L-1; omega 0.1 (AVS) / 0.7 (MVS)
+    "table3_avs1_k2_L5": ((3, 2, 4, "avs", 1, False), 29.8, 2.0),
+    "table3_mvs1_k2_L5": ((3, 2, 4, "mvs", 1, False), 9.1, 1.0),
+}
+
+
+def _gate_job(args):
+    from oracle.multigrid import solve_paper
+    n, nu, _ = solve_paper(*args)
+    return nu
+
+
+@pytest.fixture(scope="module")
+def paper_nu():
+    from concurrent.futures import ProcessPoolExecutor
+    keys = list(PAPER_GATES)
+    with ProcessPoolExecutor(min(8, len(keys))) as ex:
+        vals = list(ex.map(_gate_job, [PAPER_GATES[k][0] for k in keys]))
+    return dict(zip(keys, vals))
+
+
+@pytest.mark.parametrize("name", [k for k, v in PAPER_GATES.items() if v[1] is not None])
+def test_paper_iteration_counts(paper_nu, name):
+    """The oracle's multigrid reproduces the paper's fractional iteration counts nu."""
+    _, ref, tol = PAPER_GATES[name]
+    assert abs(paper_nu[name] - ref) <= tol, (name, paper_nu[name], ref)
+
+
+def test_paper_level_uniformity(paper_nu):
+    """convergence uniform in the mesh level -- nu(L+1) - nu(L) <= 1 (k=4, L=5 -> 6)."""
+    assert paper_nu["table2_avs2_k4_L6"] - paper_nu["table2_avs2_k4_L5"] <= 1.0

@@ -94,6 +94,24 @@ def test_energy_error_rate(k):
     assert np.all(rates >= k - 1 - 0.15)
 
 
+@pytest.mark.parametrize("d,k,Ns", [(2, 3, (4, 8, 16)), (2, 4, (4, 8, 16)), (3, 2, (2, 4, 8))])
+def test_paper_rhs_solution_is_prod_sin(d, k, Ns):
+    """the experiments' F yields the analytical solution u* = prod sin(pi x_a).  u* is not
+    clamped (d_n u* != 0), so F carries the Nitsche boundary data (reading Q8b); with it the discrete
+    solution converges to u* (nodal max error at rate >= k, one order above the energy rate k-1 of
+    Eq. energyerror) -- a sign or factor error in the boundary data stops it."""
+    from oracle.operator import paper_rhs, paper_solution
+    nod = []
+    for N in Ns:
+        s = default_sigma(k)
+        u = spla.spsolve(assemble(k, d, N, s).tocsc(), paper_rhs(k, d, N, s))
+        from oracle.operator import dof_coords
+        xs = np.meshgrid(*[dof_coords(k, N, np.arange(k * N - 1))] * d, indexing="ij")[::-1]
+        nod.append(np.abs(u - paper_solution(d)(*[x.ravel() for x in xs])).max())
+    rates = np.log2(np.array(nod[:-1]) / np.array(nod[1:]))
+    assert np.all(rates >= k - 0.3), rates          # nodal error: at least the energy rate + 1
+
+
 def test_rhs_partition_of_unity():
     k, N = 3, 4
     b = rhs_load(k, 2, N, lambda x, y: 0 * x + 2.5)
