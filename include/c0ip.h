@@ -69,7 +69,8 @@ typedef struct {
   int32_t degree;          /* k in [2,7] (Q_k)                                    */
   int32_t finest_level;    /* L >= 1: levels 1..L, N_l = 2^l (reading Q9)                      */
   int64_t cells_override;  /* 0, or N for one non-nested level (throughput runs)              */
-  double penalty_scale;    /* sigma = penalty_scale * k (k+1) (reading Q4); 0 -> 1 */
+  double penalty_scale;    /* sigma = penalty_scale * k (k+1) (reading Q4); 0 -> 1;
+                              boundary facets use 2 sigma (h_e = h/2, reading Q27)                */
   int32_t device;          /* CUDA device ordinal                                              */
 } c0ip_config;
 
@@ -107,8 +108,11 @@ c0ip_status c0ip_get_fdm(c0ip_ctx ctx, int32_t level, int32_t variant, double* S
  * (row-major; any pointer may be NULL).  ARG if n_1d > 4096. */
 c0ip_status c0ip_get_matrices_1d(c0ip_ctx ctx, int32_t level, double* M, double* L, double* B);
 
-/* b_i = int f phi_i for the paper load f = d^2 pi^4 prod sin(pi x_a) (readings Q1, Q8),
- * Gauss quadrature with k+3 points per cell and axis.  b: device FP64, length n_dofs. */
+/* F of the paper's solve experiments (readings Q1, Q8b): b_i = int f phi_i with
+ * f = Delta^2 u* = d^2 pi^4 prod sin(pi x_a), plus the Nitsche boundary data of u* = prod sin(pi x_a)
+ * (u* = 0 on the boundary, d_n u* = g != 0):  sum_{boundary facets} int g ((sigma_b/h) d_n phi_i - d_n^2 phi_i)
+ * with sigma_b = 2 sigma (reading Q27), so that the discrete solution converges to u*.  Gauss
+ * quadrature with k+3 points per cell and axis.  b: device FP64, length n_dofs. */
 c0ip_status c0ip_rhs(c0ip_ctx ctx, int32_t level, double* b, void* stream);
 
 /* y = A x with the matrix-free C0IP operator (Eqs. c0iptensorvp(3D)). */
@@ -181,7 +185,7 @@ c0ip_status c0ip_gmres(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, 
  * j = interior row + 1).  The caller fills the ghost rows of x_ext before each call (halo exchange, e.g.
  * NCCL send/recv through torch.distributed; paper_2412_05082_b200/dist.py).  Results are bitwise equal
  * to the single-domain call on the owned rows.  STATE if the level has no slab-capable kernel (2D levels
- * with N >= 8 in this release). */
+ * with N >= 8, 3D levels with N >= 8 and k <= 5 in this release). */
 
 /* Ghost rows a slab call needs on each side of [out_lo, out_hi) (clipped at the domain boundary):
  * AVS step: 4k-2 (residual on the owned rows +- (2k-2), each needing x +- 2k); apply: 2k. */

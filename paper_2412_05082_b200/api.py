@@ -34,6 +34,20 @@ def _dtype(t):
         raise ValueError(f"unsupported dtype {t.dtype}") from None
 
 
+def _check(ref, n, *ts):
+    """Every tensor: same dtype and device as `ref`, contiguous, n elements (argument marshalling
+    only; the library cannot see tensor lengths and would read/write out of bounds)."""
+    for t in (ref,) + ts:
+        if t is None:
+            continue
+        if t.dtype != ref.dtype or t.device != ref.device:
+            raise ValueError(f"tensor dtype/device {t.dtype}/{t.device} != {ref.dtype}/{ref.device}")
+        if not t.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        if t.numel() != n:
+            raise ValueError(f"tensor has {t.numel()} elements, expected {n}")
+
+
 class MG:
     """c0ip_mg_config: smoother, steps, omega, symmetric, cycle dtype (torch.float64/float32)."""
 
@@ -111,6 +125,9 @@ class Context:
     def n_dofs(self, level):
         return self.level_info(level)["n_dofs"]
 
+    def _n(self, level):
+        return self.n_dofs(level)              # the ABI rejects a bad level (C0IP_ERR_ARG)
+
     def rhs(self, level):
         b = torch.empty(self.n_dofs(level), dtype=torch.float64, device=self.device)
         L.check(self._lib.c0ip_rhs(self.h, level, _ptr(b), _stream()))
@@ -118,16 +135,19 @@ class Context:
 
     def apply(self, level, x, y=None):
         y = torch.empty_like(x) if y is None else y
+        _check(x, self._n(level), y)
         L.check(self._lib.c0ip_apply(self.h, level, _dtype(x), _ptr(x), _ptr(y), _stream()))
         return y
 
     def residual(self, level, b, x, r=None):
         r = torch.empty_like(x) if r is None else r
+        _check(x, self._n(level), b, r)
         L.check(self._lib.c0ip_residual(self.h, level, _dtype(x), _ptr(b), _ptr(x), _ptr(r), _stream()))
         return r
 
     def smooth(self, level, smoother, steps, omega, b, x, reverse=False):
         sm = SMOOTHERS[smoother] if isinstance(smoother, str) else int(smoother)
+        _check(x, self._n(level), b)
         L.check(self._lib.c0ip_smooth(self.h, level, _dtype(x), sm, int(steps), float(omega), int(bool(reverse)),
                                       _ptr(b), _ptr(x), _stream()))
         return x
@@ -135,21 +155,39 @@ class Context:
     def restrict(self, fine_level, fine, coarse=None):
         if coarse is None:
             coarse = torch.empty(self.n_dofs(fine_level - 1), dtype=fine.dtype, device=fine.device)
+        if fine_level < 2:
+            raise ValueError("restrict needs fine_level >= 2")
+        _check(fine, self._n(fine_level))
+        _check(coarse, self._n(fine_level - 1))
+        if coarse.dtype != fine.dtype or coarse.device != fine.device:
+            raise ValueError("coarse and fine tensors differ in dtype/device")
         L.check(self._lib.c0ip_restrict(self.h, fine_level, _dtype(fine), _ptr(fine), _ptr(coarse), _stream()))
         return coarse
 
     def prolongate_add(self, fine_level, coarse, fine):
+        if fine_level < 2:
+            raise ValueError("prolongate_add needs fine_level >= 2")
+        _check(fine, self._n(fine_level))
+        _check(coarse, self._n(fine_level - 1))
+        if coarse.dtype != fine.dtype or coarse.device != fine.device:
+            raise ValueError("coarse and fine tensors differ in dtype/device")
         L.check(self._lib.c0ip_prolongate_add(self.h, fine_level, _dtype(fine), _ptr(coarse), _ptr(fine),
                                               _stream()))
         return fine
 
     def vcycle(self, mg, r, z=None):
         z = torch.empty_like(r) if z is None else z
+        if r.dtype != torch.float64:
+            raise ValueError("vcycle takes FP64 vectors (the cycle dtype is set in MG)")
+        _check(r, self._n(self.finest_level), z)
         L.check(self._lib.c0ip_vcycle(self.h, C.byref(mg.c), _ptr(r), _ptr(z), _stream()))
         return z
 
     def pcg(self, mg, b, x=None, rtol=1e-8, max_iter=200):
         x = torch.zeros_like(b) if x is None else x
+        if b.dtype != torch.float64:
+            raise ValueError("pcg takes FP64 vectors")
+        _check(b, self._n(self.finest_level), x)
         rep = L.Report()
         hist = np.zeros(max_iter + 1)
         L.check(self._lib.c0ip_pcg(self.h, C.byref(mg.c), _ptr(b), _ptr(x), float(rtol), int(max_iter),
@@ -161,6 +199,9 @@ class Context:
     def gmres(self, mg, b, x=None, rtol=1e-8, max_iter=200, restart=50):
         """Flexible right-preconditioned GMRES(restart) in FP64 around the V-cycle (c0ip_gmres)."""
         x = torch.zeros_like(b) if x is None else x
+        if b.dtype != torch.float64:
+            raise ValueError("gmres takes FP64 vectors")
+        _check(b, self._n(self.finest_level), x)
         rep = L.Report()
         hist = np.zeros(max_iter + 1)
         L.check(self._lib.c0ip_gmres(self.h, C.byref(mg.c), _ptr(b), _ptr(x), float(rtol), int(max_iter),
@@ -175,13 +216,19 @@ class Context:
         L.check(self._lib.c0ip_slab_ghosts(self.h, C.byref(ga), C.byref(gp)))
         return ga.value, gp.value
 
+    def _slab_n(self, level, lrows):
+        n1 = self.level_info(level)["n_1d"]
+        return int(lrows) * n1 ** (self.dim - 1)
+
     def slab_avs_step(self, level, omega, row0, lrows, out_lo, out_hi, b_ext, x_ext, r_ext):
+        _check(x_ext, self._slab_n(level, lrows), b_ext, r_ext)
         L.check(self._lib.c0ip_slab_avs_step(self.h, level, _dtype(x_ext), float(omega), int(row0), int(lrows),
                                              int(out_lo), int(out_hi), _ptr(b_ext), _ptr(x_ext), _ptr(r_ext),
                                              _stream()))
         return x_ext
 
     def slab_apply(self, level, row0, lrows, out_lo, out_hi, x_ext, y_ext, b_ext=None):
+        _check(x_ext, self._slab_n(level, lrows), y_ext, b_ext)
         L.check(self._lib.c0ip_slab_apply(self.h, level, _dtype(x_ext), int(row0), int(lrows), int(out_lo),
                                           int(out_hi), _ptr(b_ext) if b_ext is not None else None, _ptr(x_ext),
                                           _ptr(y_ext), _stream()))

@@ -688,6 +688,10 @@ c0ip_status c0ip_destroy(c0ip_ctx ctx) {
 c0ip_status c0ip_set_path(c0ip_ctx ctx, c0ip_path path) {
   if (!ctx) return fail(C0IP_ERR_ARG, "null context");
   if (path != C0IP_PATH_AUTO && path != C0IP_PATH_GENERIC) return fail(C0IP_ERR_ARG, "bad path");
+  if (path != ctx->path && ctx->vc_exec) {       // the cached V-cycle graph was captured on the old path
+    cudaGraphExecDestroy(ctx->vc_exec);
+    ctx->vc_exec = nullptr;
+  }
   ctx->path = path;
   return C0IP_OK;
 }
@@ -778,14 +782,18 @@ c0ip_status c0ip_rhs(c0ip_ctx ctx, int32_t level, double* b, void* stream) {
   Level& L = ctx->levels[level];
   cudaStream_t st = (cudaStream_t)stream;
   std::vector<double> f1 = c0ip::sine_load_1d(ctx->k, L.N);
-  DevArr<double> tmp;
+  std::vector<double> g1 = c0ip::boundary_normal_1d(ctx->ref, L.N);
+  DevArr<double> tmp, tmpg;
   tmp.upload(f1);
+  tmpg.upload(g1);
   const double c = double(ctx->d * ctx->d) * std::pow(M_PI, 4);   // f = d^2 pi^4 prod sin (Q1, Q8)
-  c0ip::outer_load_kernel<<<grid_for(L.ndofs), 256, 0, st>>>(ctx->d, L.n, tmp.p, c, b);
+  const double cb = -M_PI;                                        // g = d_n u* = -pi prod_{b!=a} sin (Q8b)
+  c0ip::outer_load_kernel<<<grid_for(L.ndofs), 256, 0, st>>>(ctx->d, L.n, tmp.p, tmpg.p, c, cb, b);
   ctx->launches++;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
   tmp.free();
+  tmpg.free();
   return C0IP_OK;
   ABI_CATCH
 }

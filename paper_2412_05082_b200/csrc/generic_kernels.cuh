@@ -258,14 +258,18 @@ __global__ void __launch_bounds__(256) dot_final_kernel(int nparts, const double
     for (int j = 0; j < 3; ++j) out[j] = sh[j][0];
 }
 
-// b[g] = c * prod_a f1[i_a]  (separable paper load)
-__global__ void outer_load_kernel(int d, int64_t n, const double* f1, double c, double* b) {
+// b[g] = c * prod_a f1[i_a] + cb * sum_a g1[i_a] prod_{b != a} f1[i_b]
+// (separable paper load plus the separable Nitsche boundary data, reading Q8b)
+__global__ void outer_load_kernel(int d, int64_t n, const double* f1, const double* g1, double c,
+                                  double cb, double* b) {
   int64_t total = n * n * (d == 3 ? n : 1);
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
     int64_t i0 = g % n, i1 = (g / n) % n, i2 = g / (n * n);
-    double v = c * f1[i0] * f1[i1];
-    if (d == 3) v *= f1[i2];
-    b[g] = v;
+    const double f0 = f1[i0], fy = f1[i1], fz = d == 3 ? f1[i2] : 1.0;
+    double v = c * f0 * fy * fz;
+    double w = g1[i0] * fy * fz + f0 * g1[i1] * fz;
+    if (d == 3) w += f0 * fy * g1[i2];
+    b[g] = v + cb * w;
   }
 }
 

@@ -83,6 +83,7 @@ RefData make_ref(int k, double sigma) {
   RefData r;
   r.k = k;
   r.sigma = sigma;
+  r.sigma_b = kBoundaryPenalty * sigma;
   Basis1D b = make_basis(k);
   const int n1 = k + 1;
   std::vector<double> qx, qw;
@@ -131,17 +132,19 @@ void global_bands(const RefData& rd, int64_t N, Band& M, Band& L, Band& B, bool 
         add(fl, c * k + i, c * k + j, rd.Lc[i * n1 + j]);
         add(fbm, c * k + i, c * k + j, rd.Bc[i * n1 + j]);
       }
-  // face f at node f*k: (sigma/h_f) a a^T - a b^T - b a^T, h_f = h (reference: h = 1)
+  // face f at node f*k: (sigma_f/h_f) a a^T - a b^T - b a^T, h_f = h (reference: h = 1); boundary
+  // facets carry sigma_b (reading Q27)
   for (int64_t f = 0; f <= N; ++f) {
     const double *a, *b;
     int len;
     int64_t g0;
+    double sf = rd.sigma_b;
     if (f == 0) { a = rd.la.data(); b = rd.lb.data(); len = n1; g0 = 0; }
     else if (f == N) { a = rd.ua.data(); b = rd.ub.data(); len = n1; g0 = (N - 1) * k; }
-    else { a = rd.fa.data(); b = rd.fb.data(); len = 2 * k + 1; g0 = (f - 1) * k; }
+    else { a = rd.fa.data(); b = rd.fb.data(); len = 2 * k + 1; g0 = (f - 1) * k; sf = rd.sigma; }
     for (int i = 0; i < len; ++i)
       for (int j = 0; j < len; ++j)
-        add(fbm, g0 + i, g0 + j, rd.sigma * a[i] * a[j] - a[i] * b[j] - b[i] * a[j]);
+        add(fbm, g0 + i, g0 + j, sf * a[i] * a[j] - a[i] * b[j] - b[i] * a[j]);
   }
   if (!eliminate) {
     for (Band* X : {&M, &L, &B}) { X->n = nn; X->hw = hw; }
@@ -388,6 +391,19 @@ std::vector<double> sine_load_1d(int k, int64_t N) {
       b.eval(qx[q], v.data(), nullptr, nullptr);
       for (int m = 0; m <= k; ++m) full[c * k + m] += h * qw[q] * fx * v[m];
     }
+  return std::vector<double>(full.begin() + 1, full.end() - 1);
+}
+
+std::vector<double> boundary_normal_1d(const RefData& rd, int64_t N) {
+  // facet x=0: outward normal -e, d_n phi = -phi'(0)/h, d_n^2 phi = phi''(0)/h^2 (first cell's nodes);
+  // facet x=1: +e on the last cell.  la/ua hold d_n phi, lb/ub d_n^2 phi at h = 1.
+  const int k = rd.k;
+  const double h = 1.0 / double(N);
+  std::vector<double> full(k * N + 1, 0.0);
+  for (int m = 0; m <= k; ++m) {
+    full[m] += (rd.sigma_b / h) * (rd.la[m] / h) - rd.lb[m] / (h * h);
+    full[(N - 1) * k + m] += (rd.sigma_b / h) * (rd.ua[m] / h) - rd.ub[m] / (h * h);
+  }
   return std::vector<double>(full.begin() + 1, full.end() - 1);
 }
 

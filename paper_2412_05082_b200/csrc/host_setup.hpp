@@ -28,9 +28,14 @@ void gauss_legendre(int nq, std::vector<double>& x, std::vector<double>& w);   /
 
 // Reference data for one degree (h = 1).  Global matrices on N cells are
 //   M = h * Mhat,  L = Lhat / h,  B = Bhat / h^3   (all face terms included in Bhat).
+// Boundary facets: sigma/h_e with h_e = h/2 (reading Q27): the Nitsche penalty of the
+// clamped condition is twice the interior-facet penalty.
+constexpr double kBoundaryPenalty = 2.0;
+
 struct RefData {
   int k = 0;
-  double sigma = 0;
+  double sigma = 0;                        // interior facets (reading Q4)
+  double sigma_b = 0;                      // boundary facets = kBoundaryPenalty * sigma (reading Q27)
   std::vector<double> Mc, Lc, Bc;          // (k+1)^2 cell matrices, row-major
   std::vector<double> fa, fb;              // interior face: a, b over 2k+1 nodes
   std::vector<double> la, lb, ua, ub;      // boundary faces (x=0: lower, x=1: upper), k+1 nodes
@@ -78,6 +83,9 @@ bool band_is_spd(const Band& B);
 
 // 1D load f1_i = int sin(pi x) phi_i(x) dx (reference scaling: includes h), Gauss k+3 pts/cell.
 std::vector<double> sine_load_1d(int k, int64_t N);
+// 1D boundary-facet factor of the Nitsche boundary data (reading Q8b): over the interior nodes,
+// g1_i = sum_{facets x=0, x=1} ( (sigma_b/h) d_n phi_i - d_n^2 phi_i ) at the facet (physical h = 1/N).
+std::vector<double> boundary_normal_1d(const RefData& rd, int64_t N);
 
 // Cyclic Jacobi eigen-solver for a symmetric n x n matrix (row-major). Eigenvectors in columns of V.
 void jacobi_eigen(int n, std::vector<double> A, std::vector<double>& w, std::vector<double>& V);

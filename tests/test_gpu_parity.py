@@ -189,18 +189,20 @@ def test_mvs_increment(d, k, N, reverse, generic):
     ctx.set_path(False)
 
 
-# sizes spanning several fused tiles (interior fast paths, ragged last tile) of the 2D kernels
-LARGE_2D = [(2, 2, 40), (2, 3, 27), (2, 3, 32), (2, 4, 27), (2, 4, 32), (2, 5, 21), (2, 7, 13)]
+# sizes spanning several fused tiles (interior fast paths, ragged last tile) of the 2D kernels; N >= 34
+# puts more than 33 patches in a row: the atomic DMMA patch kernel's 32-patch runs get a seam
+LARGE_2D = [(2, 2, 40), (2, 3, 27), (2, 3, 32), (2, 4, 27), (2, 4, 32), (2, 5, 21), (2, 7, 13),
+            (2, 3, 36), (2, 4, 36)]
 
 
-@pytest.mark.parametrize("sm", ["avs", "mvs"])
+@pytest.mark.parametrize("sm", ["avs", "mvs", "avs_atomic"])
 @pytest.mark.parametrize("d,k,N", LARGE_2D)
 def test_smoother_increment_large_2d(d, k, N, sm):
     ctx, L = ctx_for(d, k, N)
     A, ps = oracle(d, k, N)
     x, b = random_xb(k, d, N)
-    om = 0.25 if sm == "avs" else 1.0
-    step = avs_step if sm == "avs" else mvs_step
+    om = 0.8 if sm == "mvs" else 0.25
+    step = mvs_step if sm == "mvs" else avs_step
     xt = torch.tensor(x, device=DEV)
     ctx.smooth(L, sm, 1, om, torch.tensor(b, device=DEV), xt)
     do = step(A, ps, x, b, om) - x
@@ -210,7 +212,7 @@ def test_smoother_increment_large_2d(d, k, N, sm):
     ctx.smooth(L, sm, 1, om, torch.tensor(bi, device=DEV, dtype=torch.float32), x32)
     xo32 = step(A, ps, xi, bi, om)
     xg32 = x32.cpu().numpy().astype(np.float64)
-    dtol = fp32_delta_tol(A, ps, xi, bi, om, sm)
+    dtol = fp32_delta_tol(A, ps, xi, bi, om, "mvs" if sm == "mvs" else "avs")
     assert rel(xg32 - xi, xo32 - xi) <= dtol, (rel(xg32 - xi, xo32 - xi), dtol)
     assert rel(xg32, xo32) <= max(FP32_TOL, dtol * np.linalg.norm(xo32 - xi) / np.linalg.norm(xo32))
 
@@ -422,7 +424,7 @@ def test_slab_rejects_missing_ghosts():
 
 
 # ------------------------------------------------------------------------------ 3D fused kernels (N >= 8)
-CASES_3D_FUSED = [(3, 2, 8), (3, 3, 9), (3, 4, 8), (3, 5, 8)]
+CASES_3D_FUSED = [(3, 2, 8), (3, 3, 9), (3, 4, 8), (3, 5, 8), (3, 3, 10), (3, 2, 12)]
 
 
 @pytest.mark.parametrize("d,k,N", CASES_3D_FUSED)
@@ -441,7 +443,7 @@ def test_apply_residual_3d_fused(d, k, N):
 
 
 @pytest.mark.parametrize("sm", ["avs", "avs_colored", "avs_atomic", "mvs", "mvs_rev"])
-@pytest.mark.parametrize("d,k,N", CASES_3D_FUSED[:3])
+@pytest.mark.parametrize("d,k,N", CASES_3D_FUSED)
 def test_smoothers_3d_fused(d, k, N, sm):
     ctx, L = ctx_for(d, k, N)
     ctx.set_path(False)
@@ -463,7 +465,7 @@ def test_smoothers_3d_fused(d, k, N, sm):
     ctx.smooth(L, smc, 1, om, torch.tensor(bi, device=DEV, dtype=torch.float32), x32, reverse=rev)
     xo32 = ref(xi, bi)
     xg32 = x32.cpu().numpy().astype(np.float64)
-    dtol = fp32_delta_tol(A, ps, xi, bi, om, sm)
+    dtol = fp32_delta_tol(A, ps, xi, bi, om, "mvs" if smc == "mvs" else "avs", rev)
     assert rel(xg32 - xi, xo32 - xi) <= dtol, (rel(xg32 - xi, xo32 - xi), dtol)
     assert rel(xg32, xo32) <= max(FP32_TOL, dtol * np.linalg.norm(xo32 - xi) / np.linalg.norm(xo32))
 
@@ -504,8 +506,8 @@ def _sample_ids(n, d, rng, m=48):
     return np.array(sorted(ids))
 
 
-@pytest.mark.parametrize("d,k,sm", [(2, 4, "avs_atomic"), (2, 4, "avs"), (2, 3, "avs_atomic"),
-                                    (3, 3, "avs_atomic"), (3, 2, "avs")])
+@pytest.mark.parametrize("d,k,sm", [(2, 4, "avs_atomic"), (2, 4, "avs"), (2, 3, "avs_atomic"), (2, 2, "avs_atomic"),
+                                    (3, 3, "avs_atomic"), (3, 2, "avs"), (3, 4, "avs_atomic"), (3, 5, "avs_atomic")])
 def test_full_size_sampled_avs(d, k, sm):
     from c0ip_inputs import CFG2_CELLS, CFG4_CELLS
     from oracle.smoothers import avs_delta_sample
@@ -531,3 +533,30 @@ def test_full_size_sampled_avs(d, k, sm):
     ro = np.array([residual_on_box(k, d, N, s, x, b, [(g // n ** a) % n for a in range(d)],
                                    [(g // n ** a) % n + 1 for a in range(d)])[0][0] for g in ids])
     assert np.abs(r[ids] - ro).max() <= 1e-11 * np.abs(ro).max()
+
+
+@pytest.mark.parametrize("k,sm", [(4, "avs_atomic"), (3, "avs"), (7, "avs")])
+def test_full_size_sampled_avs_fp32(k, sm):
+    """cfg2 at full size in FP32 (the mixed cycle's kernels): sampled increments against the oracle on the
+    RN-rounded inputs; bar = 4x the oracle FP32-model deviation of the same degree on a small mesh
+    (fp32_delta_tol), measured on the sample."""
+    from c0ip_inputs import CFG2_CELLS
+    from oracle.smoothers import avs_delta_sample
+    from paper_2412_05082_b200 import api
+    d, N, om = 2, CFG2_CELLS[k], 0.25
+    ctx = api.Context(d, k, 3, cells_override=N)
+    x, b = random_xb(k, d, N)
+    xi, bi = x.astype(np.float32).astype(np.float64), b.astype(np.float32).astype(np.float64)
+    n = k * N - 1
+    xt = torch.tensor(xi, device=DEV, dtype=torch.float32)
+    ctx.smooth(3, sm, 1, om, torch.tensor(bi, device=DEV, dtype=torch.float32), xt)
+    dg = xt.cpu().numpy().astype(np.float64) - xi
+    ctx.close()
+    ids = _sample_ids(n, d, np.random.default_rng(8))
+    do = avs_delta_sample(k, d, N, default_sigma(k), xi, bi, om, ids)
+    Ns = 12
+    A, ps = oracle(d, k, Ns)
+    xs, bs = random_xb(k, d, Ns)
+    xs, bs = xs.astype(np.float32).astype(np.float64), bs.astype(np.float32).astype(np.float64)
+    dtol = fp32_delta_tol(A, ps, xs, bs, om, "avs")
+    assert rel(dg[ids], do) <= dtol, (rel(dg[ids], do), dtol)
