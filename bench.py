@@ -88,6 +88,28 @@ def flops_fdm_3d(k):
     return 2.0 * 6 * np_ ** 4 / k ** 3
 
 
+def flops_matvec(d, k):
+    """canonical matvec flop/DoF (M/L rows k+2 nonzeros, B bulk k+2 plus the rank-2 face
+    part 4(2k+1)/k)."""
+    f = 4 * (2 * k + 1) / k
+    return 2.0 * (4 * (k + 2) + 2 * ((k + 2) + f)) if d == 2 else 2.0 * (9 * (k + 2) + 3 * ((k + 2) + f))
+
+
+def flops_fdm(d, k):
+    """2 * 2d (2k-1)^(d+1) / k^d flop/DoF."""
+    return 2.0 * 2 * d * (2 * k - 1) ** (d + 1) / k ** d
+
+
+def sec8d_bounds(d, k, hbm_gbs, fp64_tflops):
+    """SURVEY.md §8(d) attainable FP64 rates (GDoF/s) recomputed with the measured peaks: matvec (16 B/DoF),
+    fused AVS step (24 B/DoF, matvec + FDM flops), MVS step (U matvec + FDM flops, U = 3.2 (2D) / 4.4 (3D);
+    105 / 177 B/DoF)."""
+    mv, fdm = flops_matvec(d, k), flops_fdm(d, k)
+    U, mb = (3.2, 105.0) if d == 2 else (4.4, 177.0)
+    g = lambda byt, fl: min(hbm_gbs / byt, fp64_tflops * 1e3 / fl)
+    return {"matvec": g(16.0, mv), "avs": g(24.0, mv + fdm), "mvs": g(mb, U * mv + fdm)}
+
+
 def flops_fdm_2d(k):
     """per patch 2d (2k-1)^(d+1) MACs (S^T and S along each axis), k^-d patches per DoF."""
     np_ = 2 * k - 1
@@ -226,35 +248,57 @@ def max_over_ranks(v, world):
     return float(t.item())
 
 
-def cpu_oracle_sample(k, seconds_target=15.0, d=2):
-    """Time the CPU oracle (as it stands) on an oracle-size twin of the workload: same d and k,
-    ~0.26M DoFs (2D) / ~0.06-0.1M DoFs (3D), one AVS step (CSR residual + dense surrogate patch
-    solves).  Assembly excluded."""
+def cpu_oracle_sample(k, seconds_target=15.0, d=2, full=True):
+    """Time the CPU oracle (as it stands) on an oracle-size twin of the workload (same d and k; 2D ~0.26M
+    DoFs, 3D ~0.03-0.1M DoFs; SURVEY.md §8d / BASELINE.md "CPU baseline plan", scaled down so the whole
+    sample stays within ~30 s of CPU time): the headline value is one AVS step (CSR residual + dense
+    surrogate patch solves), beside it SpMV y = A x, one MVS step and (full=True) an MG-PCG solve to 1e-8
+    (FP64 cycle) on the nested twin mesh.  Assembly excluded from every timing."""
     import numpy as np
-    from oracle.operator import assemble
-    from oracle.smoothers import PatchSolvers, avs_step
+    from oracle.operator import assemble, paper_rhs
+    from oracle.smoothers import PatchSolvers, avs_step, mvs_step
     from oracle.discretization import default_sigma
+    from oracle.multigrid import Hierarchy, pcg, precondition, default_omega
     N = ({2: 256, 3: 170, 4: 128, 5: 102, 6: 85, 7: 73} if d == 2 else {2: 20, 3: 14, 4: 10, 5: 8})[k]
-    omega = 0.25 if d == 2 else 0.1
+    omega = default_omega(d, "avs")
     s = default_sigma(k)
     A = assemble(k, d, N, s)
     ps = PatchSolvers(k, d, N, s)
     x, b = random_xb(k, d, N)
     ndofs = len(x)
-    reps, t_total = 0, 0.0
-    while t_total < seconds_target and reps < 50:
-        t0 = time.perf_counter()
-        avs_step(A, ps, x, b, omega)
-        t_total += time.perf_counter() - t0
-        reps += 1
+
+    def rate(fn, budget):
+        reps, tot = 0, 0.0
+        while tot < budget and reps < 50:
+            t0 = time.perf_counter()
+            fn()
+            tot += time.perf_counter() - t0
+            reps += 1
+        return ndofs * reps / tot / 1e9, reps, tot
+    v_avs, r_avs, t_avs = rate(lambda: avs_step(A, ps, x, b, omega), seconds_target * 0.5)
+    v_mv, r_mv, t_mv = rate(lambda: A @ x, 2.0)
+    v_mvs, r_mvs, t_mvs = rate(lambda: mvs_step(A, ps, x, b, default_omega(d, "mvs")), seconds_target * 0.3)
     try:
         from threadpoolctl import threadpool_info
         cores = max([p.get("num_threads", 1) for p in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
-    return {"value": ndofs * reps / t_total / 1e9, "unit": "GDoF/s", "cores": cores, "kind": "oracle",
-            "sample": f"{d}D k={k} N={N} ({ndofs} DoFs), {reps} AVS step(s) in {t_total:.1f}s, CSR assembly excluded",
-            "host_cpus": os.cpu_count()}
+    out = {"value": v_avs, "unit": "GDoF/s", "cores": cores, "kind": "oracle",
+           "sample": f"{d}D k={k} N={N} ({ndofs} DoFs): {r_avs} AVS step(s) in {t_avs:.1f}s, CSR assembly excluded",
+           "host_cpus": os.cpu_count(),
+           "items": {"avs_step_gdofs": round(v_avs, 6), "spmv_gdofs": round(v_mv, 6), "spmv_cores": 1,
+                     "mvs_step_gdofs": round(v_mvs, 6)}}
+    if full:
+        Lp = {2: {2: 8, 3: 7, 4: 7, 5: 6, 6: 6, 7: 6}, 3: {2: 4, 3: 3, 4: 3, 5: 3}}[d][k]
+        h = Hierarchy(k, d, Lp, s)
+        bb = paper_rhs(k, d, 2 ** Lp, s)
+        t0 = time.perf_counter()
+        _, n, hist = pcg(h.A[Lp], bb, lambda r: precondition(h, r, "avs", 2, omega))
+        tp = time.perf_counter() - t0
+        out["items"]["mg_pcg"] = {"dofs": int(h.A[Lp].shape[0]), "level": Lp, "iterations": int(n),
+                                  "seconds": round(tp, 3), "solved_gdofs": round(h.A[Lp].shape[0] / tp / 1e9, 7),
+                                  "config": "AVS 2+2 steps, CG rtol 1e-8, FP64 cycle, paper load + boundary data"}
+    return out
 
 
 def main_smoother(d, k, dtype):
@@ -286,7 +330,7 @@ def run_reference(args):
         return
     k = args.degree
     d = args.dim
-    cb = cpu_oracle_sample(k, seconds_target=max(5.0, 20.0 / max(1, args.steps + args.warmup)), d=d)
+    cb = cpu_oracle_sample(k, seconds_target=max(5.0, 20.0 / max(1, args.steps + args.warmup)), d=d, full=False)
     line = {"metric": METRIC, "value": cb["value"], "unit": "GDoF/s", "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -399,6 +443,93 @@ def traffic_from_profiles(kernel_key):
         return None
 
 
+def _time_ms(fn, reps, stream):
+    import torch
+    fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def sweep(d, dtype, local, degrees, clk_mhz, reps=10):
+    """Degree sweep at the throughput sizes (cfg2 2D k = 2..7 / cfg4 3D k = 2..5, ~16.7M / ~50M DoFs): one
+    AVS step (the timed realisation of main_smoother), the residual alone, y = A x and one coloured MVS step,
+    each as GDoF/s and as a fraction of its SURVEY.md §8(d) FP64 bound (measured peaks).  Inputs are larger
+    than L2 (>= 3 x 134 MB)."""
+    import torch
+    from paper_2412_05082_b200 import api
+    hbm, _, _ = peaks()
+    f64 = fp64_peak_tflops(clk_mhz)
+    dt = torch.float64 if dtype == "f64" else torch.float32
+    stream = torch.cuda.current_stream()
+    out = {}
+    for k in degrees:
+        N = CFG2_CELLS[k] if d == 2 else CFG4_CELLS[k]
+        ctx = api.Context(d, k, 3, cells_override=N, device=local)
+        x0, b0 = random_xb(k, d, N)
+        x = torch.tensor(x0, device="cuda", dtype=dt)
+        b = torch.tensor(b0, device="cuda", dtype=dt)
+        r = torch.empty_like(x)
+        nd = ctx.n_dofs(3)
+        om, om_m = (0.25, 0.8) if d == 2 else (0.1, 0.7)
+        sm = main_smoother(d, k, dtype)
+        for _ in range(3):
+            ctx.smooth(3, sm, 1, om, b, x)
+        t_avs = _time_ms(lambda: ctx.smooth(3, sm, 1, om, b, x), reps, stream)
+        t_res = _time_ms(lambda: ctx.residual(3, b, x, r), reps, stream)
+        t_mv = _time_ms(lambda: ctx.apply(3, x, r), reps, stream)
+        t_mvs = _time_ms(lambda: ctx.smooth(3, "mvs", 1, om_m, b, x), max(2, reps // 4), stream)
+        bd = sec8d_bounds(d, k, hbm, f64)
+        g = lambda t: nd / (t * 1e-3) / 1e9
+        out[f"k{k}"] = {"dofs": nd, "cells": N, "avs_smoother": sm,
+                        "avs": round(g(t_avs), 3), "avs_frac": round(g(t_avs) / bd["avs"], 4),
+                        "residual_ms": round(t_res, 4), "fdm_ms": round(t_avs - t_res, 4),
+                        "matvec": round(g(t_mv), 3), "matvec_frac": round(g(t_mv) / bd["matvec"], 4),
+                        "mvs": round(g(t_mvs), 3), "mvs_frac": round(g(t_mvs) / bd["mvs"], 4),
+                        "bounds_gdofs": {kk: round(v, 1) for kk, v in bd.items()}}
+        ctx.close()
+        del x, b, r
+        torch.cuda.empty_cache()
+    out["note"] = (f"GDoF/s; *_frac = value / SURVEY.md §8(d) FP64 bound (HBM {hbm:.0f} GB/s, FP64 {f64:.1f} "
+                   f"TFLOP/s); MVS omega {0.8 if d == 2 else 0.7}, AVS omega {0.25 if d == 2 else 0.1}")
+    return out
+
+
+def mixed_3d(local):
+    """The paper's mixed-precision experiment (Fig. 4): 3D, GMRES preconditioned by the
+    V-cycle with one MVS step (omega 0.7, same-order cycle), FP64 cycle vs FP32 cycle (outer FGMRES(30) in FP64),
+    rtol 1e-8, F = c0ip_rhs, on the largest nested meshes of cfg4 (k = 2, 3: N = 128; k = 4: N = 64)."""
+    import torch
+    from paper_2412_05082_b200 import api
+    out = {}
+    for k, Lm in ((2, 7), (3, 7), (4, 6)):
+        cm = api.Context(3, k, Lm, device=local)
+        bm = cm.rhs(Lm)
+        r = {}
+        for name, cdt in (("fp64", torch.float64), ("mixed", torch.float32)):
+            mg = api.MG("mvs", 1, 0.7, symmetric=False, cycle_dtype=cdt)
+            cm.gmres(mg, bm, max_iter=2, restart=30)
+            torch.cuda.synchronize()
+            xs, rep, hist = cm.gmres(mg, bm, max_iter=60, restart=30)
+            r[name] = {"seconds": round(rep["seconds"], 4), "iterations": rep["iterations"],
+                       "nu": round(rep["nu"], 2), "converged": rep["converged"],
+                       "solved_mdofs_per_s": round(cm.n_dofs(Lm) / rep["seconds"] / 1e6, 1)}
+        r["dofs"] = cm.n_dofs(Lm)
+        r["mixed_speedup"] = round(r["fp64"]["seconds"] / r["mixed"]["seconds"], 3)
+        out[f"k{k}_L{Lm}"] = r
+        cm.close()
+        del bm
+        torch.cuda.empty_cache()
+    out["config"] = ("3D unit cube, MVS 1+1 step omega=0.7 (16 colours, same order), FGMRES(30) rtol 1e-8, x0=0, "
+                     "paper load + Nitsche boundary data; FP32 cycle = every level and table in FP32, conversion at "
+                     "the cycle's entry and exit (PAPER.md:749)")
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -410,6 +541,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--dim", type=int, default=2, choices=[2, 3])
+    ap.add_argument("--no-sweep", action="store_true", help="skip the 2D/3D degree sweeps")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -665,6 +797,11 @@ def main():
     else:
         ctx.close()
 
+    if not args.no_pcg and world == 1 and d == 2:
+        line["mixed_3d"] = mixed_3d(local)
+    if not args.no_sweep and world == 1:
+        line["sweep_2d"] = sweep(2, args.dtype, local, range(2, 8), clk_mhz)
+        line["sweep_3d_cfg4"] = sweep(3, args.dtype, local, range(2, 6), clk_mhz, reps=4)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_oracle_sample(k, d=d)
     if rank == 0:

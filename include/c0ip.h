@@ -83,6 +83,17 @@ c0ip_status c0ip_destroy(c0ip_ctx ctx);
 const char* c0ip_last_error(void);
 c0ip_status c0ip_set_path(c0ip_ctx ctx, c0ip_path path);
 
+/* Local solver of the vertex-patch smoothers (applies to c0ip_smooth, c0ip_vcycle, c0ip_pcg, c0ip_gmres):
+ *  FDM    the separable surrogate A~_v = sum_a B_a (x) M_others solved by fast diagonalisation
+ *         (Eq. localsolverbila; the default, Table 2/3);
+ *  EXACT  the exact patch matrix A_v = R_v A R_v^T (Table 1), built per
+ *         patch variant tuple from the 1D blocks (Eqs. c0iptensorvp(3D)), inverted densely in FP64 on the host
+ *         on first use (C0IP_ERR_COERCIVITY if an A_v is not SPD) and applied as a fused gather / DMMA GEMM /
+ *         scatter-add (device memory: n_tuples (2k-1)^(2d) doubles per level, owned by the ctx).
+ * ARG for an unknown value. */
+typedef enum { C0IP_LOCAL_FDM = 0, C0IP_LOCAL_EXACT = 1 } c0ip_local_solver;
+c0ip_status c0ip_set_local_solver(c0ip_ctx ctx, c0ip_local_solver solver);
+
 /* Level geometry.  n_dofs = (kN-1)^d, n_1d = kN-1, cells = N, n_patches = (N-1)^d,
  * n_colors = 2^(d+1).  Any output pointer may be NULL. */
 c0ip_status c0ip_level_info(c0ip_ctx ctx, int32_t level, int64_t* n_dofs, int64_t* n_1d,

@@ -23,6 +23,9 @@ class Config(C.Structure):
                 ("cells_override", C.c_int64), ("penalty_scale", C.c_double), ("device", C.c_int32)]
 
 
+LOCAL_FDM, LOCAL_EXACT = 0, 1
+
+
 class MgConfig(C.Structure):
     _fields_ = [("smoother", C.c_int), ("steps", C.c_int32), ("omega", C.c_double),
                 ("symmetric", C.c_int32), ("cycle_dtype", C.c_int)]
@@ -38,6 +41,7 @@ EXPORTS = {
     "c0ip_destroy": (C.c_int, [C.c_void_p]),
     "c0ip_last_error": (C.c_char_p, []),
     "c0ip_set_path": (C.c_int, [C.c_void_p, C.c_int]),
+    "c0ip_set_local_solver": (C.c_int, [C.c_void_p, C.c_int]),
     "c0ip_level_info": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                   C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "c0ip_patch_dofs": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]),

@@ -83,6 +83,10 @@ class Context:
     def set_path(self, generic):
         L.check(self._lib.c0ip_set_path(self.h, L.PATH_GENERIC if generic else L.PATH_AUTO))
 
+    def set_local_solver(self, exact):
+        """FDM surrogate (default, Eq. localsolverbila) or exact patch matrices A_v (Table 1)."""
+        L.check(self._lib.c0ip_set_local_solver(self.h, L.LOCAL_EXACT if exact else L.LOCAL_FDM))
+
     def level_info(self, level):
         nd, n1, nc, npch = (C.c_int64() for _ in range(4))
         ncol = C.c_int32()

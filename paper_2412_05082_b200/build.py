@@ -15,7 +15,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
           "--expt-relaxed-constexpr"]
 
-SOURCES = ["c0ip.cu", "fused_kernels.cu", "fused3d.cu", "transfer2d.cu", "mma2d.cu", "host_setup.cpp"]
+SOURCES = ["c0ip.cu", "fused_kernels.cu", "fused3d.cu", "transfer2d.cu", "mma2d.cu", "exact_local.cu", "host_setup.cpp"]
 
 
 def _compile(src):

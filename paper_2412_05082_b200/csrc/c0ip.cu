@@ -18,6 +18,7 @@
 #include "generic_kernels.cuh"
 #include "fused_dispatch.hpp"
 #include "host_setup.hpp"
+#include "exact_local.hpp"
 
 namespace {
 thread_local std::string g_err;
@@ -82,6 +83,23 @@ struct Tables {
   DevArr<T> vx, vb, vr;               // V-cycle vectors
 };
 
+struct ExactDev {                     // exact local solvers of one level
+  c0ip::ExactHost host;
+  std::vector<DevArr<double>> inv64;
+  std::vector<DevArr<float>> inv32;
+  DevArr<int64_t> off;
+  std::vector<DevArr<int32_t>> all;                 // per tuple
+  std::vector<std::vector<DevArr<int32_t>>> by_color;   // [colour][tuple]
+  ~ExactDev() {
+    for (auto& a : inv64) a.free();
+    for (auto& a : inv32) a.free();
+    off.free();
+    for (auto& a : all) a.free();
+    for (auto& c : by_color)
+      for (auto& a : c) a.free();
+  }
+};
+
 struct Level {
   int l = 0;
   int64_t N = 0, n = 0, ndofs = 0, npatch = 0;
@@ -98,6 +116,7 @@ struct Level {
   std::vector<int64_t> parity_off;
   DevArr<int32_t> colors_d, parity_d;
   std::unique_ptr<c0ip::FusedLevel, c0ip::FusedLevelDeleter> fused;
+  std::unique_ptr<ExactDev> exact;    // built on first use of the exact local solver
 };
 
 }  // namespace
@@ -108,6 +127,7 @@ struct c0ip_ctx_s {
   double sigma = 0;
   int lmin = 1, lmax = 1;
   c0ip_path path = C0IP_PATH_AUTO;
+  c0ip_local_solver local = C0IP_LOCAL_FDM;
   c0ip::RefData ref;
   std::vector<Level> levels;          // index = level number (entries < lmin unused)
   int64_t launches = 0;
@@ -135,6 +155,7 @@ struct c0ip_ctx_s {
       for (int i = 0; i < 4; ++i) { L.t64.S[i].free(); L.t64.lam[i].free(); L.t32.S[i].free(); L.t32.lam[i].free(); }
       L.Elo.free(); L.Etlo.free(); L.colors_d.free(); L.parity_d.free();
       L.fused.reset();
+      L.exact.reset();
     }
     pcg_r.free(); pcg_z.free(); pcg_p.free(); pcg_Ap.free(); dot_part.free(); dot_out.free();
     gm_V.free(); gm_Z.free(); gm_w.free();
@@ -332,12 +353,76 @@ void disjoint_patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, con
   patch_solve<T>(ctx, L, r, x, omega, list, count, 0, st);
 }
 
+ExactDev& exact_tables(c0ip_ctx ctx, Level& L) {
+  if (!L.exact) {
+    std::unique_ptr<ExactDev> e(new ExactDev());
+    const int nc = 1 << (ctx->d + 1);
+    std::vector<int32_t> col(L.npatch);
+    for (int c = 0; c < nc; ++c)
+      for (int64_t i = L.color_off[c]; i < L.color_off[c + 1]; ++i) col[L.colors_h[i]] = c;
+    std::string err;
+    if (!c0ip::build_exact_host(ctx->d, ctx->k, L.N, L.M, L.L, L.B, col, nc, e->host, err))
+      throw std::runtime_error("coercivity: " + err);
+    const size_t nt = e->host.tuples.size();
+    e->inv64.resize(nt); e->inv32.resize(nt); e->all.resize(nt);
+    for (size_t i = 0; i < nt; ++i) {
+      e->inv64[i].upload(e->host.inv[i]);
+      e->inv32[i].upload(cast_vec<float>(e->host.inv[i]));
+      e->all[i].upload(e->host.all[i]);
+    }
+    e->by_color.resize(nc);
+    for (int c = 0; c < nc; ++c) {
+      e->by_color[c].resize(nt);
+      for (size_t i = 0; i < nt; ++i) e->by_color[c][i].upload(e->host.by_color[c][i]);
+    }
+    e->off.upload(e->host.off);
+    L.exact = std::move(e);
+  }
+  return *L.exact;
+}
+
+// x += omega sum_{v in lists} R_v^T A_v^{-1} R_v r with the exact local matrices (fused gather / DMMA GEMM /
+// scatter-add per variant tuple, exact_local.cu)
+template <typename T>
+void exact_patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, int color, cudaStream_t st) {
+  ExactDev& e = exact_tables(ctx, L);
+  for (size_t i = 0; i < e.host.tuples.size(); ++i) {
+    const auto& lst = color < 0 ? e.all[i] : e.by_color[color][i];
+    const int64_t cnt = color < 0 ? (int64_t)e.host.all[i].size() : (int64_t)e.host.by_color[color][i].size();
+    if (cnt == 0) continue;
+    c0ip::ExactArgs<T> a;
+    if constexpr (std::is_same<T, double>::value) a.Ainv = e.inv64[i].p; else a.Ainv = e.inv32[i].p;
+    a.nloc = e.host.nloc; a.off = e.off.p; a.list = lst.p; a.count = cnt;
+    a.d = ctx->d; a.k = ctx->k; a.N = L.N; a.n = L.n; a.r = r; a.x = x; a.omega = omega;
+    c0ip::launch_exact_patches<T>(a, st);
+    ctx->launches++;
+    CK(cudaGetLastError());
+  }
+}
+
 template <typename T>
 void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, bool reverse,
                  const T* b, T* x, cudaStream_t st) {
   Tables<T>& t = tab<T>(L);
   t.sres.alloc(L.ndofs);
   const int d = ctx->d;
+  if (ctx->local == C0IP_LOCAL_EXACT) {        // exact local solvers
+    for (int s = 0; s < steps; ++s) {
+      if (sm == C0IP_MVS) {
+        const int nc = 1 << (d + 1);
+        for (int ci = 0; ci < nc; ++ci) {
+          const int c = reverse ? nc - 1 - ci : ci;
+          if (L.color_off[c + 1] == L.color_off[c]) continue;
+          apply_op<T>(ctx, L, x, b, t.sres.p, st);
+          exact_patch_solve<T>(ctx, L, t.sres.p, x, omega, c, st);
+        }
+      } else {                                   // every AVS realisation: one residual, atomic scatter-add
+        apply_op<T>(ctx, L, x, b, t.sres.p, st);
+        exact_patch_solve<T>(ctx, L, t.sres.p, x, omega, -1, st);
+      }
+    }
+    return;
+  }
   for (int s = 0; s < steps; ++s) {
     if (sm == C0IP_MVS) {
       const int nc = 1 << (d + 1);
@@ -515,6 +600,8 @@ void vcycle_graph(c0ip_ctx ctx, const c0ip_mg_config& mg, const double* r, doubl
     if (ctx->vc_exec) { cudaGraphExecDestroy(ctx->vc_exec); ctx->vc_exec = nullptr; }
     if (!ctx->cap_stream) CK(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
     CK(cudaStreamSynchronize(st));
+    if (ctx->local == C0IP_LOCAL_EXACT)           // tables uploaded before capture (no copies inside it)
+      for (int l = ctx->lmin; l <= ctx->lmax; ++l) exact_tables(ctx, ctx->levels[l]);
     const int64_t l0 = ctx->launches;
     CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
     try {
@@ -693,6 +780,17 @@ c0ip_status c0ip_set_path(c0ip_ctx ctx, c0ip_path path) {
     ctx->vc_exec = nullptr;
   }
   ctx->path = path;
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_set_local_solver(c0ip_ctx ctx, c0ip_local_solver solver) {
+  if (!ctx) return fail(C0IP_ERR_ARG, "null context");
+  if (solver != C0IP_LOCAL_FDM && solver != C0IP_LOCAL_EXACT) return fail(C0IP_ERR_ARG, "bad local solver");
+  if (solver != ctx->local && ctx->vc_exec) {     // the cached V-cycle graph was captured with the old solver
+    cudaGraphExecDestroy(ctx->vc_exec);
+    ctx->vc_exec = nullptr;
+  }
+  ctx->local = solver;
   return C0IP_OK;
 }
 

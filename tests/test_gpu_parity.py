@@ -560,3 +560,58 @@ def test_full_size_sampled_avs_fp32(k, sm):
     xs, bs = xs.astype(np.float32).astype(np.float64), bs.astype(np.float32).astype(np.float64)
     dtol = fp32_delta_tol(A, ps, xs, bs, om, "avs")
     assert rel(dg[ids], do) <= dtol, (rel(dg[ids], do), dtol)
+
+
+# ------------------------------------------------------------------------------ exact local solvers
+EXACT_CASES = [(2, 2, 8), (2, 3, 5), (2, 4, 8), (2, 5, 3), (3, 2, 4), (3, 3, 3), (2, 2, 2), (3, 2, 2)]
+
+
+@pytest.mark.parametrize("sm", ["avs_atomic", "mvs", "mvs_rev"])
+@pytest.mark.parametrize("d,k,N", EXACT_CASES)
+def test_exact_local_smoothers(d, k, N, sm):
+    """c0ip_set_local_solver(EXACT): the smoother with A_v = R_v A R_v^T (Table 1) against the
+    oracle's dense exact patch solves (PatchSolvers(exact_A=A)); FP64 1e-11, FP32 at the FP32-model bar."""
+    from paper_2412_05082_b200 import api
+    L = int(np.log2(N)) if 2 ** int(np.log2(N)) == N else 3
+    ctx = api.Context(d, k, L, cells_override=0 if 2 ** int(np.log2(N)) == N else N)
+    ctx.set_local_solver(True)
+    A = assemble(k, d, N, default_sigma(k))
+    ps = PatchSolvers(k, d, N, default_sigma(k), exact_A=A)
+    x, b = random_xb(k, d, N)
+    rev = sm == "mvs_rev"
+    kind = "mvs" if sm.startswith("mvs") else "avs"
+    om = (0.8 if d == 2 else 0.7) if kind == "mvs" else (0.25 if d == 2 else 0.1)
+    ref = (lambda xi, bi: mvs_step(A, ps, xi, bi, om, reverse=rev)) if kind == "mvs" else \
+        (lambda xi, bi: avs_step(A, ps, xi, bi, om))
+    xt = torch.tensor(x, device=DEV)
+    ctx.smooth(L, kind if kind == "mvs" else sm, 1, om, torch.tensor(b, device=DEV), xt, reverse=rev)
+    assert rel(xt.cpu().numpy() - x, ref(x, b) - x) <= FP64_TOL
+    xi, bi = x.astype(np.float32).astype(np.float64), b.astype(np.float32).astype(np.float64)
+    x32 = torch.tensor(xi, device=DEV, dtype=torch.float32)
+    ctx.smooth(L, kind if kind == "mvs" else sm, 1, om, torch.tensor(bi, device=DEV, dtype=torch.float32), x32,
+               reverse=rev)
+    dtol = fp32_delta_tol(A, ps, xi, bi, om, kind, rev)
+    assert rel(x32.cpu().numpy().astype(np.float64) - xi, ref(xi, bi) - xi) <= dtol
+    ctx.close()
+
+
+@pytest.mark.parametrize("kind,steps", [("avs", 2), ("mvs", 1)])
+def test_exact_local_table1_iterations(kind, steps):
+    """Table 1: 2D k=4 L=6 with exact local solvers -- the GPU solve within 1 iteration of the
+    oracle's (paper protocol: CG + AVS-2 omega 1/4, GMRES + MVS-1 omega 1) and nu within 1 of the paper."""
+    from paper_2412_05082_b200 import api
+    from oracle.multigrid import solve_paper
+    d, k, L = 2, 4, 6
+    no, nuo, _ = solve_paper(d, k, L, kind, steps, exact=True)
+    ctx = api.Context(d, k, L)
+    ctx.set_local_solver(True)
+    b = ctx.rhs(L)
+    if kind == "avs":
+        x, rep, hist = ctx.pcg(api.MG("avs", steps, 0.25), b)
+        paper = 10.3
+    else:
+        x, rep, hist = ctx.gmres(api.MG("mvs", steps, 1.0, symmetric=False), b)
+        paper = 2.9
+    assert rep["converged"] and abs(rep["iterations"] - no) <= 1, (rep, no)
+    assert abs(rep["nu"] - paper) <= 1.0
+    ctx.close()
