@@ -214,6 +214,47 @@ c0ip_status c0ip_slab_apply(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, int64_t 
                             int64_t out_lo, int64_t out_hi, const void* b_ext, const void* x_ext,
                             void* y_ext, void* stream);
 
+/* One colour of the multiplicative smoother on a slab (SURVEY.md §8e "colours are processed in
+ * lockstep across ranks"): every patch of `color` whose DoF rows meet the owned node rows [out_lo, out_hi) is
+ * solved (residual on its footprint, FDM, update of its DoFs).  Patches straddling a slab boundary are solved
+ * redundantly by both neighbours from identical inputs, so after the call the owned rows equal the single-domain
+ * colour step bitwise; rows outside the owned range are ghost copies (refresh them by the next exchange).  The
+ * caller exchanges the 4k-2 ghost rows of x_ext before every colour.  r_ext: scratch of the window's size.
+ * ARG: bad colour / window; STATE with the exact local solver. */
+c0ip_status c0ip_slab_mvs_color(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, double omega, int32_t color,
+                                int64_t row0, int64_t lrows, int64_t out_lo, int64_t out_hi, const void* b_ext,
+                                void* x_ext, void* r_ext, void* stream);
+
+/* Windowed transfers between a nested level pair: coarse node rows [c_out_lo, c_out_hi) of
+ * P^T fine from a fine window (restrict), and fine node rows [f_out_lo, f_out_hi) += P coarse from a coarse
+ * window (prolongate_add).  Windows as above (row0 = global interior row of local row 0, lrows rows).
+ * c0ip_slab_transfer_rows reports the node-row ranges [need[0], need[1]) each call reads (fine rows for the
+ * restriction of the coarse owned rows, coarse rows for the prolongation onto the fine owned rows).
+ * ARG if a window misses rows it needs; STATE without a coarser nested level. */
+c0ip_status c0ip_slab_restrict(c0ip_ctx ctx, int32_t fine_level, c0ip_dtype dt, int64_t f_row0, int64_t f_lrows,
+                               const void* fine_ext, int64_t c_row0, int64_t c_lrows, int64_t c_out_lo,
+                               int64_t c_out_hi, void* coarse_ext, void* stream);
+c0ip_status c0ip_slab_prolongate_add(c0ip_ctx ctx, int32_t fine_level, c0ip_dtype dt, int64_t c_row0,
+                                     int64_t c_lrows, const void* coarse_ext, int64_t f_row0, int64_t f_lrows,
+                                     int64_t f_out_lo, int64_t f_out_hi, void* fine_ext, void* stream);
+c0ip_status c0ip_slab_transfer_rows(c0ip_ctx ctx, int32_t fine_level, int64_t c_out_lo, int64_t c_out_hi,
+                                    int64_t f_out_lo, int64_t f_out_hi, int64_t* fine_need, int64_t* coarse_need);
+
+/* z = MG_level(0, r) (Algorithm 1 from an inner level): the replicated coarse part of the
+ * distributed V-cycle (every rank runs it on the gathered coarse residual).  r, z: device FP64 of n_dofs(level);
+ * the cycle dtype conversion as in c0ip_vcycle.  Not graph-captured. */
+c0ip_status c0ip_vcycle_level(c0ip_ctx ctx, const c0ip_mg_config* mg, int32_t level, const double* r, double* z,
+                              void* stream);
+
+/* Vector kernels of the distributed Krylov drivers (the solver arithmetic stays in this library):
+ * y = alpha x + beta y (n elements, device, dtype dt; beta = 0 does not read y), and up to two FP64 dot
+ * products <x0,y0>, <x1,y1> over n elements (deterministic two-pass reduction; out: host array of ndots,
+ * the call synchronises the stream).  The cross-rank sum is the caller's all-reduce. */
+c0ip_status c0ip_vec_axpby(c0ip_ctx ctx, c0ip_dtype dt, int64_t n, double alpha, const void* x, double beta,
+                          void* y, void* stream);
+c0ip_status c0ip_vec_dots(c0ip_ctx ctx, int64_t n, int32_t ndots, const double* x0, const double* y0,
+                          const double* x1, const double* y1, double* out, void* stream);
+
 /* Number of kernels this context has launched since creation (for the bench's gpu_launches). */
 c0ip_status c0ip_launch_count(c0ip_ctx ctx, int64_t* count);
 

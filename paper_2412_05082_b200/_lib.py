@@ -63,6 +63,20 @@ EXPORTS = {
     "c0ip_gmres": (C.c_int, [C.c_void_p, C.POINTER(MgConfig), C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
                              C.c_int32, C.POINTER(Report), C.c_void_p, C.c_void_p]),
     "c0ip_launch_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "c0ip_slab_mvs_color": (C.c_int, [C.c_void_p, C.c_int32, C.c_int, C.c_double, C.c_int32, C.c_int64, C.c_int64,
+                                      C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "c0ip_slab_restrict": (C.c_int, [C.c_void_p, C.c_int32, C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                     C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
+    "c0ip_slab_prolongate_add": (C.c_int, [C.c_void_p, C.c_int32, C.c_int, C.c_int64, C.c_int64, C.c_void_p,
+                                           C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
+    "c0ip_slab_transfer_rows": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_int64,
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "c0ip_vec_axpby": (C.c_int, [C.c_void_p, C.c_int, C.c_int64, C.c_double, C.c_void_p, C.c_double, C.c_void_p,
+                                 C.c_void_p]),
+    "c0ip_vec_dots": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_void_p]),
+    "c0ip_vcycle_level": (C.c_int, [C.c_void_p, C.POINTER(MgConfig), C.c_int32, C.c_void_p, C.c_void_p,
+                                    C.c_void_p]),
     "c0ip_slab_ghosts": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "c0ip_slab_avs_step": (C.c_int, [C.c_void_p, C.c_int32, C.c_int, C.c_double, C.c_int64, C.c_int64, C.c_int64,
                                      C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -237,3 +237,60 @@ class Context:
                                           int(out_hi), _ptr(b_ext) if b_ext is not None else None, _ptr(x_ext),
                                           _ptr(y_ext), _stream()))
         return y_ext
+
+    def slab_mvs_color(self, level, omega, color, row0, lrows, out_lo, out_hi, b_ext, x_ext, r_ext):
+        _check(x_ext, self._slab_n(level, lrows), b_ext, r_ext)
+        L.check(self._lib.c0ip_slab_mvs_color(self.h, level, _dtype(x_ext), float(omega), int(color), int(row0),
+                                              int(lrows), int(out_lo), int(out_hi), _ptr(b_ext), _ptr(x_ext),
+                                              _ptr(r_ext), _stream()))
+        return x_ext
+
+    def slab_restrict(self, fine_level, f_row0, f_lrows, fine_ext, c_row0, c_lrows, c_out_lo, c_out_hi, coarse_ext):
+        _check(fine_ext, self._slab_n(fine_level, f_lrows))
+        _check(coarse_ext, self._slab_n(fine_level - 1, c_lrows))
+        L.check(self._lib.c0ip_slab_restrict(self.h, fine_level, _dtype(fine_ext), int(f_row0), int(f_lrows),
+                                             _ptr(fine_ext), int(c_row0), int(c_lrows), int(c_out_lo), int(c_out_hi),
+                                             _ptr(coarse_ext), _stream()))
+        return coarse_ext
+
+    def slab_prolongate_add(self, fine_level, c_row0, c_lrows, coarse_ext, f_row0, f_lrows, f_out_lo, f_out_hi,
+                            fine_ext):
+        _check(fine_ext, self._slab_n(fine_level, f_lrows))
+        _check(coarse_ext, self._slab_n(fine_level - 1, c_lrows))
+        L.check(self._lib.c0ip_slab_prolongate_add(self.h, fine_level, _dtype(fine_ext), int(c_row0), int(c_lrows),
+                                                   _ptr(coarse_ext), int(f_row0), int(f_lrows), int(f_out_lo),
+                                                   int(f_out_hi), _ptr(fine_ext), _stream()))
+        return fine_ext
+
+    def slab_transfer_rows(self, fine_level, c_out_lo, c_out_hi, f_out_lo, f_out_hi):
+        fn, cn = (C.c_int64 * 2)(), (C.c_int64 * 2)()
+        L.check(self._lib.c0ip_slab_transfer_rows(self.h, fine_level, int(c_out_lo), int(c_out_hi), int(f_out_lo),
+                                                  int(f_out_hi), fn, cn))
+        return (fn[0], fn[1]), (cn[0], cn[1])
+
+    def vcycle_level(self, mg, level, r, z=None):
+        z = torch.empty_like(r) if z is None else z
+        if r.dtype != torch.float64:
+            raise ValueError("vcycle_level takes FP64 vectors")
+        _check(r, self._n(level), z)
+        L.check(self._lib.c0ip_vcycle_level(self.h, C.byref(mg.c), int(level), _ptr(r), _ptr(z), _stream()))
+        return z
+
+    def axpby(self, alpha, x, beta, y):
+        """y = alpha x + beta y (library kernel; x, y same dtype/device/length)."""
+        _check(x, x.numel(), y)
+        L.check(self._lib.c0ip_vec_axpby(self.h, _dtype(x), x.numel(), float(alpha), _ptr(x), float(beta), _ptr(y),
+                                         _stream()))
+        return y
+
+    def dots(self, x0, y0, x1=None, y1=None):
+        """[<x0,y0>] or [<x0,y0>, <x1,y1>] in FP64 (library kernels, synchronises)."""
+        if x0.dtype != torch.float64:
+            raise ValueError("dots takes FP64 vectors")
+        _check(x0, x0.numel(), y0, x1, y1)
+        nd = 1 if x1 is None else 2
+        out = np.zeros(nd)
+        L.check(self._lib.c0ip_vec_dots(self.h, x0.numel(), nd, _ptr(x0), _ptr(y0), _ptr(x1) if x1 is not None else None,
+                                        _ptr(y1) if y1 is not None else None, out.ctypes.data_as(C.c_void_p),
+                                        _stream()))
+        return out

@@ -7,7 +7,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <tuple>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -83,6 +85,12 @@ struct Tables {
   DevArr<T> vx, vb, vr;               // V-cycle vectors
 };
 
+struct WinLists {                     // slab: patches whose DoF rows meet the owned node rows, per colour
+  std::vector<std::vector<int32_t>> h;
+  std::vector<DevArr<int32_t>> dev;
+  ~WinLists() { for (auto& a : dev) a.free(); }
+};
+
 struct ExactDev {                     // exact local solvers of one level
   c0ip::ExactHost host;
   std::vector<DevArr<double>> inv64;
@@ -128,6 +136,7 @@ struct c0ip_ctx_s {
   int lmin = 1, lmax = 1;
   c0ip_path path = C0IP_PATH_AUTO;
   c0ip_local_solver local = C0IP_LOCAL_FDM;
+  std::map<std::tuple<int, int64_t, int64_t>, std::unique_ptr<WinLists>> wins;   // slab MVS patch lists
   c0ip::RefData ref;
   std::vector<Level> levels;          // index = level number (entries < lmin unused)
   int64_t launches = 0;
@@ -209,6 +218,10 @@ c0ip::LineOp<T> square_op(const DevArr<T>& band, int k, int64_t n) {
 template <typename T>
 void launch_axis(c0ip_ctx ctx, const c0ip::AxisArgs<T>& a, cudaStream_t st) {
   int64_t total = a.dims[0] * a.dims[1] * a.dims[2];
+  if (a.sax >= 0) {
+    if (a.scnt <= 0) return;
+    total = total / a.dims[a.sax] * a.scnt;
+  }
   c0ip::axis_apply_kernel<T><<<grid_for(total), 256, 0, st>>>(a);
   ctx->launches++;
   CK(cudaGetLastError());
@@ -224,6 +237,9 @@ c0ip::AxisArgs<T> axis_args(int64_t n0, int64_t n1, int64_t n2, int axis, T* out
   a.gamma = 0;
   a.beta = 0;
   a.out = out;
+  a.sax = -1;
+  a.s0 = 0;
+  a.scnt = 0;
   return a;
 }
 
@@ -242,21 +258,31 @@ void ensure_tmp(Level& L, int d) {
   for (int i = 0; i < need; ++i) t.tmp[i].alloc(L.ndofs);
 }
 
-// y = A x, or r = b - A x if b != nullptr (sum factorisation; Eqs. c0iptensorvp(3D))
+// y = A x, or r = b - A x if b != nullptr (sum factorisation; Eqs. c0iptensorvp(3D)).
+// Rows: only the slow-axis interior rows [jlo, jhi) of y are written (default: all); x, b, y are indexed
+// globally (a slab window passes pointers shifted by -row0 * row), the per-axis temporaries are full-size
+// level arrays of which only the rows the last stage reads ([jlo - 2k, jhi + 2k)) are computed.
 template <typename T>
-void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStream_t st) {
+void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStream_t st, int64_t jlo = 0,
+                   int64_t jhi = -1) {
   const int d = ctx->d, k = ctx->k;
   const int64_t n = L.n;
+  if (jhi < 0) jhi = n;
+  if (jhi <= jlo) return;
   Tables<T>& t = tab<T>(L);
   ensure_tmp<T>(L, d);
   auto Mo = square_op(t.M, k, n), Lo = square_op(t.L, k, n), Bo = square_op(t.B, k, n);
   const int64_t n2 = (d == 3) ? n : 1;
+  const int sax = d - 1;                                         // slowest axis
+  const int64_t tlo = std::max<int64_t>(0, jlo - 2 * k), thi = std::min<int64_t>(n, jhi + 2 * k);
+  auto rows = [&](c0ip::AxisArgs<T>& a, int64_t lo, int64_t hi) { a.sax = sax; a.s0 = lo; a.scnt = hi - lo; };
   // x-stage: B_x x, L_x x, M_x x
   {
     const c0ip::LineOp<T>* ops[3] = {&Bo, &Lo, &Mo};
     for (int i = 0; i < 3; ++i) {
       auto a = axis_args<T>(n, n, n2, 0, t.tmp[i].p);
       add_term(a, x, *ops[i], T(1));
+      rows(a, tlo, thi);
       launch_axis(ctx, a, st);
     }
   }
@@ -268,6 +294,7 @@ void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStr
     add_term(a, (const T*)t.tmp[1].p, Lo, T(2) * sg);
     add_term(a, (const T*)t.tmp[2].p, Bo, sg);
     if (b) { a.z = b; a.gamma = T(1); }
+    rows(a, jlo, jhi);
     launch_axis(ctx, a, st);
     return;
   }
@@ -277,13 +304,16 @@ void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStr
     add_term(a, (const T*)t.tmp[0].p, Mo, T(1));
     add_term(a, (const T*)t.tmp[2].p, Bo, T(1));
     add_term(a, (const T*)t.tmp[1].p, Lo, T(2));
+    rows(a, tlo, thi);
     launch_axis(ctx, a, st);
     auto q = axis_args<T>(n, n, n, 1, t.tmp[4].p);
     add_term(q, (const T*)t.tmp[2].p, Lo, T(1));
     add_term(q, (const T*)t.tmp[1].p, Mo, T(1));
+    rows(q, tlo, thi);
     launch_axis(ctx, q, st);
     auto r = axis_args<T>(n, n, n, 1, t.tmp[5].p);
     add_term(r, (const T*)t.tmp[2].p, Mo, T(1));
+    rows(r, tlo, thi);
     launch_axis(ctx, r, st);
   }
   // z-stage: y = M_z P + 2 L_z Q + B_z R
@@ -292,6 +322,7 @@ void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStr
   add_term(a, (const T*)t.tmp[4].p, Lo, T(2) * sg);
   add_term(a, (const T*)t.tmp[5].p, Bo, sg);
   if (b) { a.z = b; a.gamma = T(1); }
+  rows(a, jlo, jhi);
   launch_axis(ctx, a, st);
 }
 
@@ -571,16 +602,17 @@ void vcycle_rec(c0ip_ctx ctx, int l, const c0ip_mg_config& mg, T* x, const T* b,
                  mg.symmetric && mg.smoother == C0IP_MVS, b, x, st);
 }
 
-void vcycle_top(c0ip_ctx ctx, const c0ip_mg_config& mg, const double* r, double* z, cudaStream_t st) {
-  Level& L = ctx->levels[ctx->lmax];
+void vcycle_top(c0ip_ctx ctx, const c0ip_mg_config& mg, const double* r, double* z, cudaStream_t st, int level = -1) {
+  const int l = level < 0 ? ctx->lmax : level;
+  Level& L = ctx->levels[l];
   if (mg.cycle_dtype == C0IP_F64) {
-    vcycle_rec<double>(ctx, ctx->lmax, mg, z, r, st);
+    vcycle_rec<double>(ctx, l, mg, z, r, st);
   } else {
     Tables<float>& t = L.t32;
     t.vx.alloc(L.ndofs);
     t.vb.alloc(L.ndofs);
     convert<double, float>(ctx, L.ndofs, r, t.vb.p, st);    // conversion at V-cycle entry
-    vcycle_rec<float>(ctx, ctx->lmax, mg, t.vx.p, t.vb.p, st);
+    vcycle_rec<float>(ctx, l, mg, t.vx.p, t.vb.p, st);
     convert<float, double>(ctx, L.ndofs, t.vx.p, z, st);
   }
 }
@@ -1242,6 +1274,298 @@ c0ip_status c0ip_slab_apply(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, int64_t 
     slab_apply_impl<float>(ctx, L, (const float*)x_ext, (const float*)b_ext, (float*)y_ext, w, st);
   else
     return fail(C0IP_ERR_ARG, "bad dtype");
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------- slab extension
+// Colour-lockstep MVS, windowed transfers and the V-cycle from an inner level: the pieces of the
+// distributed V-cycle / Krylov solvers (paper_2412_05082_b200/dist.py drives them).
+// Window convention as above: x_ext[(j - 1 - row0) * row + ...] holds node row j of the slow axis.  Kernels
+// that index the level globally get "virtual" pointers x_ext - row0 * row; they only touch rows inside the
+// window (checked by the callers' ghost widths).
+namespace {
+
+int64_t slow_row_len(const c0ip_ctx ctx, const Level& L) { return ctx->d == 2 ? L.n : L.n * L.n; }
+
+std::map<std::tuple<int, int64_t, int64_t>, std::unique_ptr<WinLists>>& win_cache(c0ip_ctx ctx) {
+  return ctx->wins;
+}
+
+WinLists& win_lists(c0ip_ctx ctx, Level& L, int64_t out_lo, int64_t out_hi) {
+  auto key = std::make_tuple(L.l, out_lo, out_hi);
+  auto& cache = win_cache(ctx);
+  auto it = cache.find(key);
+  if (it != cache.end()) return *it->second;
+  std::unique_ptr<WinLists> w(new WinLists());
+  const int nc = 1 << (ctx->d + 1), k = ctx->k;
+  w->h.assign(nc, {});
+  int64_t stride = 1;
+  for (int a = 0; a < ctx->d - 1; ++a) stride *= (L.N - 1);
+  for (int c = 0; c < nc; ++c)
+    for (int64_t i = L.color_off[c]; i < L.color_off[c + 1]; ++i) {
+      const int32_t p = L.colors_h[i];
+      const int64_t vs = 1 + p / stride;                       // slow-axis vertex of the patch
+      if ((vs + 1) * k - 1 >= out_lo && (vs - 1) * k + 1 <= out_hi - 1) w->h[c].push_back(p);
+    }
+  w->dev.resize(nc);
+  for (int c = 0; c < nc; ++c) w->dev[c].upload(w->h[c]);
+  WinLists& ref = *w;
+  cache[key] = std::move(w);
+  return ref;
+}
+
+// one MVS colour on a slab: residual on the colour's patches (footprint), FDM solve, update of their DoFs
+// (owned rows +- (k-1); rows outside the owned range are ghost copies refreshed by the next exchange)
+template <typename T>
+void slab_mvs_color_impl(c0ip_ctx ctx, Level& L, int color, T omega, int64_t row0, int64_t lrows, int64_t out_lo,
+                         int64_t out_hi, const T* b_ext, T* x_ext, T* r_ext, cudaStream_t st) {
+  WinLists& wl = win_lists(ctx, L, out_lo, out_hi);
+  const int64_t cnt = (int64_t)wl.h[color].size();
+  if (cnt == 0) return;
+  const int32_t* list = wl.dev[color].p;
+  const int64_t row = slow_row_len(ctx, L);
+  const T* bv = b_ext - row0 * row;
+  T* xv = x_ext - row0 * row;
+  T* rv = r_ext - row0 * row;
+  const int k = ctx->k;
+  if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 2 &&
+      c0ip::fused_mvs_color<T>(*L.fused, list, cnt, omega, bv, xv, st, &ctx->launches))
+    return;
+  if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
+      c0ip::fused3_mvs_color<T>(*L.fused, list, cnt, omega, bv, xv, st, &ctx->launches))
+    return;
+  // residual on the patch DoF rows: node rows [out_lo - (k-1), out_hi + k - 1] (the slab cuts are vertex rows);
+  // the same kernel as the single-domain step (fused apply3d on the window, else the generic per-axis kernels)
+  const int64_t KN = int64_t(k) * L.N;
+  const c0ip::SlabWindow wr{row0, lrows, std::max<int64_t>(1, out_lo - (k - 1)), std::min<int64_t>(KN, out_hi + k)};
+  if (!(ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
+        c0ip::fused3_apply<T>(*L.fused, x_ext, b_ext, r_ext, st, &ctx->launches, &wr)))
+    generic_apply<T>(ctx, L, xv, bv, rv, st, wr.out_lo - 1, wr.out_hi - 1);
+  if (ctx->local == C0IP_LOCAL_EXACT) throw std::runtime_error("slab MVS with exact local solvers is not supported");
+  if (mma_patches<T>(ctx, L, rv, xv, omega, list, cnt, 0, st)) return;
+  if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
+      c0ip::fused3_patch_fdm<T>(*L.fused, omega, rv, xv, list, cnt, st, &ctx->launches, 0))
+    return;
+  patch_solve<T>(ctx, L, rv, xv, omega, list, cnt, 0, st);
+}
+
+// coarse node rows [c_out_lo, c_out_hi) of P^T fine (restriction) from a fine window
+template <typename T>
+void slab_restrict_impl(c0ip_ctx ctx, Level& F, const T* fv, T* cv, int64_t ic_lo, int64_t ic_hi, cudaStream_t st) {
+  Tables<T>& t = tab<T>(F);
+  ensure_tmp<T>(F, ctx->d);
+  const int64_t nf = F.n, nc = F.E.cols;
+  const int width = F.Et.width;
+  const int64_t fr_lo = F.Et.lo[ic_lo], fr_hi = F.Et.lo[ic_hi - 1] + width;
+  c0ip::LineOp<T> Et;
+  Et.v = t.Et.p; Et.lo = F.Etlo.p; Et.width = width; Et.hw = 0; Et.n_in = nf;
+  if (ctx->d == 2) {
+    auto a = axis_args<T>(nc, nf, 1, 0, t.tmp[0].p);
+    add_term(a, fv, Et, T(1));
+    a.sax = 1; a.s0 = fr_lo; a.scnt = fr_hi - fr_lo;
+    launch_axis(ctx, a, st);
+    auto b = axis_args<T>(nc, nc, 1, 1, cv);
+    add_term(b, (const T*)t.tmp[0].p, Et, T(1));
+    b.sax = 1; b.s0 = ic_lo; b.scnt = ic_hi - ic_lo;
+    launch_axis(ctx, b, st);
+    return;
+  }
+  auto a = axis_args<T>(nc, nf, nf, 0, t.tmp[0].p);
+  add_term(a, fv, Et, T(1));
+  a.sax = 2; a.s0 = fr_lo; a.scnt = fr_hi - fr_lo;
+  launch_axis(ctx, a, st);
+  auto b = axis_args<T>(nc, nc, nf, 1, t.tmp[1].p);
+  add_term(b, (const T*)t.tmp[0].p, Et, T(1));
+  b.sax = 2; b.s0 = fr_lo; b.scnt = fr_hi - fr_lo;
+  launch_axis(ctx, b, st);
+  auto c = axis_args<T>(nc, nc, nc, 2, cv);
+  add_term(c, (const T*)t.tmp[1].p, Et, T(1));
+  c.sax = 2; c.s0 = ic_lo; c.scnt = ic_hi - ic_lo;
+  launch_axis(ctx, c, st);
+}
+
+// fine interior rows [if_lo, if_hi) += (P coarse) (prolongation = embedding)
+template <typename T>
+void slab_prolongate_impl(c0ip_ctx ctx, Level& F, const T* cv, T* fv, int64_t if_lo, int64_t if_hi, cudaStream_t st) {
+  Tables<T>& t = tab<T>(F);
+  ensure_tmp<T>(F, ctx->d);
+  const int64_t nf = F.n, nc = F.E.cols;
+  const int width = F.E.width;
+  const int64_t cr_lo = F.E.lo[if_lo], cr_hi = F.E.lo[if_hi - 1] + width;
+  c0ip::LineOp<T> E;
+  E.v = t.E.p; E.lo = F.Elo.p; E.width = width; E.hw = 0; E.n_in = nc;
+  if (ctx->d == 2) {
+    auto a = axis_args<T>(nf, nc, 1, 0, t.tmp[0].p);
+    add_term(a, cv, E, T(1));
+    a.sax = 1; a.s0 = cr_lo; a.scnt = cr_hi - cr_lo;
+    launch_axis(ctx, a, st);
+    auto b = axis_args<T>(nf, nf, 1, 1, fv);
+    add_term(b, (const T*)t.tmp[0].p, E, T(1));
+    b.beta = T(1);
+    b.sax = 1; b.s0 = if_lo; b.scnt = if_hi - if_lo;
+    launch_axis(ctx, b, st);
+    return;
+  }
+  auto a = axis_args<T>(nf, nc, nc, 0, t.tmp[0].p);
+  add_term(a, cv, E, T(1));
+  a.sax = 2; a.s0 = cr_lo; a.scnt = cr_hi - cr_lo;
+  launch_axis(ctx, a, st);
+  auto b = axis_args<T>(nf, nf, nc, 1, t.tmp[1].p);
+  add_term(b, (const T*)t.tmp[0].p, E, T(1));
+  b.sax = 2; b.s0 = cr_lo; b.scnt = cr_hi - cr_lo;
+  launch_axis(ctx, b, st);
+  auto c = axis_args<T>(nf, nf, nf, 2, fv);
+  add_term(c, (const T*)t.tmp[1].p, E, T(1));
+  c.beta = T(1);
+  c.sax = 2; c.s0 = if_lo; c.scnt = if_hi - if_lo;
+  launch_axis(ctx, c, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+c0ip_status c0ip_slab_mvs_color(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, double omega, int32_t color,
+                                int64_t row0, int64_t lrows, int64_t out_lo, int64_t out_hi, const void* b_ext,
+                                void* x_ext, void* r_ext, void* stream) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (!b_ext || !x_ext || !r_ext) return fail(C0IP_ERR_ARG, "null vector");
+  if (color < 0 || color >= (1 << (ctx->d + 1))) return fail(C0IP_ERR_ARG, "bad colour");
+  Level& L = ctx->levels[level];
+  if ((s = check_window(ctx, L, row0, lrows, out_lo, out_hi, 4 * ctx->k - 2))) return s;
+  ABI_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dt == C0IP_F64)
+    slab_mvs_color_impl<double>(ctx, L, color, omega, row0, lrows, out_lo, out_hi, (const double*)b_ext,
+                                (double*)x_ext, (double*)r_ext, st);
+  else if (dt == C0IP_F32)
+    slab_mvs_color_impl<float>(ctx, L, color, (float)omega, row0, lrows, out_lo, out_hi, (const float*)b_ext,
+                               (float*)x_ext, (float*)r_ext, st);
+  else
+    return fail(C0IP_ERR_ARG, "bad dtype");
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_slab_restrict(c0ip_ctx ctx, int32_t fine_level, c0ip_dtype dt, int64_t f_row0, int64_t f_lrows,
+                               const void* fine_ext, int64_t c_row0, int64_t c_lrows, int64_t c_out_lo,
+                               int64_t c_out_hi, void* coarse_ext, void* stream) {
+  c0ip_status s = check_level(ctx, fine_level);
+  if (s) return s;
+  if (fine_level - 1 < ctx->lmin || ctx->cfg.cells_override > 0) return fail(C0IP_ERR_STATE, "no coarser level");
+  if (!fine_ext || !coarse_ext) return fail(C0IP_ERR_ARG, "null vector");
+  Level& F = ctx->levels[fine_level];
+  Level& Cl = ctx->levels[fine_level - 1];
+  const int64_t ic_lo = c_out_lo - 1, ic_hi = c_out_hi - 1;      // interior coarse rows
+  if (ic_lo < 0 || ic_hi > Cl.n || ic_lo >= ic_hi) return fail(C0IP_ERR_ARG, "coarse rows outside the level");
+  if (c_row0 < 0 || c_row0 > ic_lo || c_row0 + c_lrows < ic_hi) return fail(C0IP_ERR_ARG, "coarse window");
+  const int64_t fr_lo = F.Et.lo[ic_lo], fr_hi = F.Et.lo[ic_hi - 1] + F.Et.width;
+  if (f_row0 > fr_lo || f_row0 + f_lrows < std::min<int64_t>(fr_hi, F.n))
+    return fail(C0IP_ERR_ARG, "fine window lacks the rows the restriction reads (need interior rows [" +
+                                  std::to_string(fr_lo) + ", " + std::to_string(fr_hi) + "))");
+  ABI_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rf = slow_row_len(ctx, F), rc = slow_row_len(ctx, Cl);
+  if (dt == C0IP_F64)
+    slab_restrict_impl<double>(ctx, F, (const double*)fine_ext - f_row0 * rf, (double*)coarse_ext - c_row0 * rc,
+                               ic_lo, ic_hi, st);
+  else if (dt == C0IP_F32)
+    slab_restrict_impl<float>(ctx, F, (const float*)fine_ext - f_row0 * rf, (float*)coarse_ext - c_row0 * rc,
+                              ic_lo, ic_hi, st);
+  else
+    return fail(C0IP_ERR_ARG, "bad dtype");
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_slab_prolongate_add(c0ip_ctx ctx, int32_t fine_level, c0ip_dtype dt, int64_t c_row0,
+                                     int64_t c_lrows, const void* coarse_ext, int64_t f_row0, int64_t f_lrows,
+                                     int64_t f_out_lo, int64_t f_out_hi, void* fine_ext, void* stream) {
+  c0ip_status s = check_level(ctx, fine_level);
+  if (s) return s;
+  if (fine_level - 1 < ctx->lmin || ctx->cfg.cells_override > 0) return fail(C0IP_ERR_STATE, "no coarser level");
+  if (!fine_ext || !coarse_ext) return fail(C0IP_ERR_ARG, "null vector");
+  Level& F = ctx->levels[fine_level];
+  Level& Cl = ctx->levels[fine_level - 1];
+  const int64_t if_lo = f_out_lo - 1, if_hi = f_out_hi - 1;
+  if (if_lo < 0 || if_hi > F.n || if_lo >= if_hi) return fail(C0IP_ERR_ARG, "fine rows outside the level");
+  if (f_row0 < 0 || f_row0 > if_lo || f_row0 + f_lrows < if_hi) return fail(C0IP_ERR_ARG, "fine window");
+  const int64_t cr_lo = F.E.lo[if_lo], cr_hi = F.E.lo[if_hi - 1] + F.E.width;
+  if (c_row0 > cr_lo || c_row0 + c_lrows < std::min<int64_t>(cr_hi, Cl.n))
+    return fail(C0IP_ERR_ARG, "coarse window lacks the rows the prolongation reads (need interior rows [" +
+                                  std::to_string(cr_lo) + ", " + std::to_string(cr_hi) + "))");
+  ABI_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rf = slow_row_len(ctx, F), rc = slow_row_len(ctx, Cl);
+  if (dt == C0IP_F64)
+    slab_prolongate_impl<double>(ctx, F, (const double*)coarse_ext - c_row0 * rc, (double*)fine_ext - f_row0 * rf,
+                                 if_lo, if_hi, st);
+  else if (dt == C0IP_F32)
+    slab_prolongate_impl<float>(ctx, F, (const float*)coarse_ext - c_row0 * rc, (float*)fine_ext - f_row0 * rf,
+                                if_lo, if_hi, st);
+  else
+    return fail(C0IP_ERR_ARG, "bad dtype");
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_vcycle_level(c0ip_ctx ctx, const c0ip_mg_config* mg, int32_t level, const double* r, double* z,
+                              void* stream) {
+  c0ip_status s = check_mg(ctx, mg);
+  if (s) return s;
+  if ((s = check_level(ctx, level))) return s;
+  if (!r || !z) return fail(C0IP_ERR_ARG, "null vector");
+  ABI_TRY
+  vcycle_top(ctx, *mg, r, z, (cudaStream_t)stream, level);
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_slab_transfer_rows(c0ip_ctx ctx, int32_t fine_level, int64_t c_out_lo, int64_t c_out_hi,
+                                    int64_t f_out_lo, int64_t f_out_hi, int64_t* fine_need, int64_t* coarse_need) {
+  c0ip_status s = check_level(ctx, fine_level);
+  if (s) return s;
+  if (fine_level - 1 < ctx->lmin || ctx->cfg.cells_override > 0) return fail(C0IP_ERR_STATE, "no coarser level");
+  Level& F = ctx->levels[fine_level];
+  Level& Cl = ctx->levels[fine_level - 1];
+  const int64_t ic_lo = c_out_lo - 1, ic_hi = c_out_hi - 1, if_lo = f_out_lo - 1, if_hi = f_out_hi - 1;
+  if (ic_lo < 0 || ic_hi > Cl.n || ic_lo >= ic_hi || if_lo < 0 || if_hi > F.n || if_lo >= if_hi)
+    return fail(C0IP_ERR_ARG, "rows outside the level");
+  if (fine_need) {            // node rows of the fine vector the restriction of [c_out_lo, c_out_hi) reads
+    fine_need[0] = F.Et.lo[ic_lo] + 1;
+    fine_need[1] = std::min<int64_t>(F.Et.lo[ic_hi - 1] + F.Et.width, F.n) + 1;
+  }
+  if (coarse_need) {          // node rows of the coarse vector the prolongation onto [f_out_lo, f_out_hi) reads
+    coarse_need[0] = F.E.lo[if_lo] + 1;
+    coarse_need[1] = std::min<int64_t>(F.E.lo[if_hi - 1] + F.E.width, Cl.n) + 1;
+  }
+  return C0IP_OK;
+}
+
+c0ip_status c0ip_vec_axpby(c0ip_ctx ctx, c0ip_dtype dt, int64_t n, double alpha, const void* x, double beta,
+                          void* y, void* stream) {
+  if (!ctx || !x || !y || n < 0) return fail(C0IP_ERR_ARG, "null argument / negative length");
+  ABI_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) return C0IP_OK;
+  if (dt == C0IP_F64) axpby<double>(ctx, n, alpha, (const double*)x, beta, (double*)y, st);
+  else if (dt == C0IP_F32) axpby<float>(ctx, n, (float)alpha, (const float*)x, (float)beta, (float*)y, st);
+  else return fail(C0IP_ERR_ARG, "bad dtype");
+  return C0IP_OK;
+  ABI_CATCH
+}
+
+c0ip_status c0ip_vec_dots(c0ip_ctx ctx, int64_t n, int32_t ndots, const double* x0, const double* y0,
+                          const double* x1, const double* y1, double* out, void* stream) {
+  if (!ctx || !out || !x0 || !y0 || n < 0 || ndots < 1 || ndots > 2 || (ndots == 2 && (!x1 || !y1)))
+    return fail(C0IP_ERR_ARG, "bad dot arguments");
+  ABI_TRY
+  if (n == 0) { for (int i = 0; i < ndots; ++i) out[i] = 0.0; return C0IP_OK; }
+  dots(ctx, n, ndots, x0, y0, x1, y1, nullptr, nullptr, out, (cudaStream_t)stream);
   return C0IP_OK;
   ABI_CATCH
 }

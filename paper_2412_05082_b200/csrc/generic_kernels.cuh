@@ -31,19 +31,25 @@ struct AxisArgs {
   T gamma;
   T beta;                 // out = beta * out + ... (beta != 0 reads out)
   T* out;
+  int sax;                // slab range: iterate only c[sax] in [s0, s0 + scnt) (sax < 0: every index)
+  int64_t s0, scnt;
 };
 
 // out[idx] = beta*out + gamma*z + sum_t alpha_t * sum_q op_t(i_a, q) * in_t[idx with i_a -> col]
 // Sum factorisation of PAPER.md:344 (one 1D contraction per launch and term).
 template <typename T>
 __global__ void __launch_bounds__(256) axis_apply_kernel(AxisArgs<T> a) {
-  const int64_t total = a.dims[0] * a.dims[1] * a.dims[2];
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
+  int64_t it[3] = {a.dims[0], a.dims[1], a.dims[2]};
+  if (a.sax >= 0) it[a.sax] = a.scnt;
+  const int64_t total = it[0] * it[1] * it[2];
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
     int64_t c[3];
-    c[0] = idx % a.dims[0];
-    c[1] = (idx / a.dims[0]) % a.dims[1];
-    c[2] = idx / (a.dims[0] * a.dims[1]);
+    c[0] = q % it[0];
+    c[1] = (q / it[0]) % it[1];
+    c[2] = q / (it[0] * it[1]);
+    if (a.sax >= 0) c[a.sax] += a.s0;
+    const int64_t idx = c[0] + a.dims[0] * (c[1] + a.dims[1] * c[2]);
     T acc = 0;
     for (int t = 0; t < a.nterms; ++t) {
       const LineOp<T>& op = a.op[t];

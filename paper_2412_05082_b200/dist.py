@@ -81,3 +81,213 @@ def exchange_ghosts(x_ext, slab, row_len, group=None):
         for req in dist.batch_isend_irecv(ops):
             req.wait()
     return recv_bytes
+
+
+# ----------------------------------------------------------------------------------------------------------
+# Distributed multigrid and Krylov drivers.  Every computation is a C-ABI call on the rank's
+# window (c0ip_slab_* for the distributed levels, c0ip_vcycle_level for the replicated coarse part,
+# c0ip_vec_axpby / c0ip_vec_dots for the Krylov vectors); torch.distributed carries the ghost-row exchanges
+# (one per smoothing step / MVS colour / residual / transfer), the coarse-level all-gather (agglomeration) and
+# the all-reduced dot products.  On one GPU per rank the group is NCCL; the 2-rank tests run both ranks on one
+# GPU with gloo, staging the exchanged rows through host memory.
+
+def _host_staged(t):
+    import torch.distributed as dist
+    return t.is_cuda and dist.get_backend() == "gloo"
+
+
+def exchange(x_ext, slab, row_len, group=None):
+    """exchange_ghosts, with gloo + CUDA tensors staged through host memory (both ranks on one GPU)."""
+    if slab.nranks == 1:
+        return 0
+    if not _host_staged(x_ext):
+        return exchange_ghosts(x_ext, slab, row_len, group)
+    h = x_ext.cpu()
+    nbytes = exchange_ghosts(h, slab, row_len, group)
+    rows, hrows = x_ext.view(-1, row_len), h.view(-1, row_len)
+    lo, hi = slab.own_lo - slab.win_lo, slab.own_hi - slab.win_lo
+    if lo > 0:
+        rows[:lo].copy_(hrows[:lo])
+    if hi < rows.shape[0]:
+        rows[hi:].copy_(hrows[hi:])
+    return nbytes
+
+
+def allreduce_sum(vals, device, group=None):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(list(vals), dtype=torch.float64)
+    if dist.get_backend() != "gloo":
+        t = t.to(device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return [float(v) for v in t.cpu()]
+
+
+class DistLevel:
+    def __init__(self, ctx, level, nranks, rank, ghost, dtype, device):
+        import torch
+        info = ctx.level_info(level)
+        self.level, self.N, self.n = level, info["cells"], info["n_1d"]
+        self.k, self.d = ctx.degree, ctx.dim
+        self.row = self.n ** (self.d - 1)
+        self.slab = partition(self.N, self.k, nranks, ghost)[rank]
+        self.slabs = partition(self.N, self.k, nranks, ghost)
+        size = self.slab.lrows * self.row
+        self.x, self.b, self.r = (torch.zeros(size, dtype=dtype, device=device) for _ in range(3))
+
+    def owned(self, v):
+        return v.view(-1, self.row)[self.slab.own_local].reshape(-1)
+
+
+class DistMG:
+    """The V-cycle of Algorithm 1 on slabs: levels L, L-1, ... stay distributed while every
+    rank owns at least `min_cells` cells of the level (single-hop halos) and the level has the fused slab
+    kernels (N >= 8); below, the restricted residual is all-gathered (agglomeration) and every rank runs the
+    remaining coarse cycle redundantly (c0ip_vcycle_level, deterministic), then prolongates onto its own rows.
+    FP64 cycle (the FP32 cycle's data conversion happens inside the replicated part only)."""
+
+    def __init__(self, ctx, mg_kind="avs", steps=2, omega=0.25, symmetric=True, group=None, min_cells=4):
+        import torch
+        import torch.distributed as dist
+        from . import api
+        self.ctx, self.group = ctx, group
+        self.rank, self.nranks = dist.get_rank(group), dist.get_world_size(group)
+        self.kind, self.steps, self.omega, self.symmetric = mg_kind, steps, omega, symmetric
+        self.device = ctx.device
+        k, d = ctx.degree, ctx.dim
+        self.ghost = 4 * k - 2
+        self.levels = {}
+        lvl = ctx.finest_level
+        while lvl > 1:
+            N = ctx.level_info(lvl)["cells"]
+            if N < 8 or N // self.nranks < max(min_cells, 1) or N % self.nranks:
+                break
+            self.levels[lvl] = DistLevel(ctx, lvl, self.nranks, self.rank, self.ghost, torch.float64, self.device)
+            lvl -= 1
+        if not self.levels:
+            raise ValueError("the finest level is too small to distribute over this many ranks")
+        self.lowest = min(self.levels)
+        self.coarse_mg = api.MG(mg_kind, steps, omega, symmetric=symmetric)
+        self.ncolors = 2 ** (d + 1)
+        nc = ctx.level_info(self.lowest - 1)["n_dofs"]
+        self.c_full = torch.zeros(nc, dtype=torch.float64, device=self.device)
+        self.e_full = torch.zeros(nc, dtype=torch.float64, device=self.device)
+        self.exchanges = 0
+
+    def _xchg(self, lev, v):
+        self.exchanges += 1
+        exchange(v, lev.slab, lev.row, self.group)
+
+    def smooth(self, lev, x, b, reverse=False):
+        s = lev.slab
+        for _ in range(self.steps):
+            if self.kind == "mvs":
+                order = range(self.ncolors - 1, -1, -1) if reverse else range(self.ncolors)
+                for c in order:
+                    self._xchg(lev, x)
+                    self.ctx.slab_mvs_color(lev.level, self.omega, c, s.row0, s.lrows, s.own_lo, s.own_hi, b, x, lev.r)
+            else:
+                self._xchg(lev, x)
+                self.ctx.slab_avs_step(lev.level, self.omega, s.row0, s.lrows, s.own_lo, s.own_hi, b, x, lev.r)
+
+    def residual(self, lev, x, b, r):
+        """owned rows of r = b - A x (ghosts of x exchanged first)"""
+        s = lev.slab
+        self._xchg(lev, x)
+        self.ctx.slab_apply(lev.level, s.row0, s.lrows, s.own_lo, s.own_hi, x, r, b_ext=b)
+
+    def apply(self, lev, x, y):
+        s = lev.slab
+        self._xchg(lev, x)
+        self.ctx.slab_apply(lev.level, s.row0, s.lrows, s.own_lo, s.own_hi, x, y)
+
+    def _gather_coarse(self, lev_c_level, part_rows, src):
+        """all-gather the owned coarse node rows [lo, hi) of every rank into self.c_full"""
+        import torch
+        import torch.distributed as dist
+        info = self.ctx.level_info(lev_c_level)
+        n, row = info["n_1d"], info["n_1d"] ** (self.ctx.dim - 1)
+        cells = info["cells"]
+        parts = partition(cells, self.ctx.degree, self.nranks, 0)
+        mx = max(p.own_hi - p.own_lo for p in parts) * row
+        mine = parts[self.rank]
+        buf = torch.zeros(mx, dtype=torch.float64, device=self.device)
+        buf[: (mine.own_hi - mine.own_lo) * row] = src.view(-1, row)[mine.own_lo - 1: mine.own_hi - 1].reshape(-1)
+        staged = _host_staged(buf)
+        sendb = buf.cpu() if staged else buf
+        outs = [torch.zeros_like(sendb) for _ in range(self.nranks)]
+        dist.all_gather(outs, sendb, group=self.group)
+        full = self.c_full.view(-1, row)
+        for p, o in zip(parts, outs):
+            full[p.own_lo - 1: p.own_hi - 1] = o[: (p.own_hi - p.own_lo) * row].view(-1, row).to(self.device)
+        return parts
+
+    def cycle(self, level, x, b):
+        """x = MG_level(0, b) on the rank's window of a distributed level (owned rows valid on return)."""
+        lev = self.levels[level]
+        s = lev.slab
+        x.zero_()
+        self._xchg(lev, b)                               # the smoothers read b on the patch rows beyond the owned ones
+        self.smooth(lev, x, b)
+        self.residual(lev, x, b, lev.r)
+        self._xchg(lev, lev.r)                           # the restriction reads fine rows below the owned ones
+        if level - 1 in self.levels:
+            cl = self.levels[level - 1]
+            cs = cl.slab
+            self.ctx.slab_restrict(level, s.row0, s.lrows, lev.r, cs.row0, cs.lrows, cs.own_lo, cs.own_hi, cl.b)
+            self.cycle(level - 1, cl.x, cl.b)
+            self._xchg(cl, cl.x)                         # the prolongation reads coarse rows around the owned ones
+            self.ctx.slab_prolongate_add(level, cs.row0, cs.lrows, cl.x, s.row0, s.lrows, s.own_lo, s.own_hi, x)
+        else:
+            info = self.ctx.level_info(level - 1)
+            nc = info["n_1d"]
+            parts = partition(info["cells"], self.ctx.degree, self.nranks, 0)
+            mine = parts[self.rank]
+            self.c_full.zero_()
+            self.ctx.slab_restrict(level, s.row0, s.lrows, lev.r, 0, nc, mine.own_lo, mine.own_hi, self.c_full)
+            self._gather_coarse(level - 1, None, self.c_full)
+            self.ctx.vcycle_level(self.coarse_mg, level - 1, self.c_full, self.e_full)
+            self.ctx.slab_prolongate_add(level, 0, nc, self.e_full, s.row0, s.lrows, s.own_lo, s.own_hi, x)
+        self.smooth(lev, x, b, reverse=self.symmetric and self.kind == "mvs")
+        return x
+
+
+class DistPCG:
+    """MG-preconditioned CG in FP64 on slabs (Saad Alg. 9.1 as c0ip_pcg): vectors are windows of
+    the finest level, the update arithmetic runs in the library (c0ip_vec_axpby / c0ip_vec_dots on the owned rows),
+    dot products are all-reduced, the preconditioner is DistMG.cycle."""
+
+    def __init__(self, mgd):
+        self.m = mgd
+        self.lev = mgd.levels[mgd.ctx.finest_level]
+
+    def dot2(self, a, b, c=None, d=None):
+        o = self.lev.owned
+        v = self.m.ctx.dots(o(a), o(b)) if c is None else self.m.ctx.dots(o(a), o(b), o(c), o(d))
+        return allreduce_sum(v, self.m.device, self.m.group)
+
+    def solve(self, b_ext, rtol=1e-8, max_iter=200):
+        import torch
+        ctx, lev, o = self.m.ctx, self.lev, self.lev.owned
+        x = torch.zeros_like(b_ext)
+        r, z, p, Ap = (torch.zeros_like(b_ext) for _ in range(4))
+        self.m.residual(lev, x, b_ext, r)
+        self.m.cycle(lev.level, z, r)
+        ctx.axpby(1.0, o(z), 0.0, o(p))
+        rz, rr = self.dot2(r, z, r, r)
+        hist = [rr ** 0.5]
+        n = 0
+        while n < max_iter and hist[-1] > rtol * hist[0]:
+            self.m.apply(lev, p, Ap)
+            alpha = rz / self.dot2(p, Ap)[0]
+            ctx.axpby(alpha, o(p), 1.0, o(x))
+            ctx.axpby(-alpha, o(Ap), 1.0, o(r))
+            n += 1
+            hist.append(self.dot2(r, r)[0] ** 0.5)
+            if hist[-1] <= rtol * hist[0]:
+                break
+            self.m.cycle(lev.level, z, r)
+            rz_new = self.dot2(r, z)[0]
+            ctx.axpby(1.0, o(z), rz_new / rz, o(p))
+            rz = rz_new
+        return x, n, hist
