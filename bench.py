@@ -222,13 +222,22 @@ def ramp_until(fn, seconds):
 
 
 def dist_setup(args):
+    """One process per GPU over NCCL.  Test knobs (never used for bench numbers): C0IP_BENCH_BACKEND=gloo and
+    C0IP_BENCH_ONE_GPU=1 run every rank on cuda:0 with host-staged halos (exercises the N > 1 code path on a
+    one-GPU box)."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("C0IP_BENCH_ONE_GPU"):
+        local = 0
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("C0IP_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -243,7 +252,7 @@ def max_over_ranks(v, world):
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if dist.get_backend() == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -349,7 +358,7 @@ def run_slabs(args, world, rank, local):
     import torch
     import torch.distributed as dist
     from paper_2412_05082_b200 import api
-    from paper_2412_05082_b200.dist import partition, exchange_ghosts
+    from paper_2412_05082_b200.dist import partition, exchange as exchange_ghosts
     k, d = args.degree, args.dim
     N1 = CFG2_CELLS[k] if d == 2 else (128 if k == 3 else CFG4_CELLS[k])
     N = int(round(N1 * world ** (1.0 / d)))
@@ -428,10 +437,68 @@ def run_slabs(args, world, rank, local):
         "e2e": {"value": round(total_dofs / (t_e2e * 1e-3) / 1e9, 3), "unit": "GDoF/s",
                 "h2d_bytes_per_step": 2 * own_rows * row * esz, "d2h_bytes_per_step": own_rows * row * esz},
     }
+    # one coloured MVS step on the slabs: colours in lockstep, one ghost exchange per colour
+    om_m = 0.8 if d == 2 else 0.7
+
+    def mvs_step():
+        for c in range(2 ** (d + 1)):
+            exchange_ghosts(xw, s, row)
+            ctx.slab_mvs_color(L, om_m, c, s.row0, s.lrows, s.own_lo, s.own_hi, bw, xw, rw)
+    mvs_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    mreps = max(2, args.steps // 4)
+    e0.record(stream)
+    for _ in range(mreps):
+        mvs_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_mvs = max_over_ranks(e0.elapsed_time(e1) / mreps, world)
+    line["mvs"] = {"value": round(total_dofs / (t_mvs * 1e-3) / 1e9, 3), "unit": "GDoF/s", "ms": round(t_mvs, 4),
+                   "note": f"one coloured MVS step, {2 ** (d + 1)} colours in lockstep, omega={om_m}"}
+    ctx.close()
+    del xw, bw, rw
+    torch.cuda.empty_cache()
+    if not args.no_pcg:
+        line["pcg_strong"] = dist_pcg(args, world, rank, local)
     if rank == 0:
         print(json.dumps(line))
-    ctx.close()
     dist.destroy_process_group()
+
+
+def dist_pcg(args, world, rank, local):
+    """MG-PCG time-to-solve on slabs (strong scaling: one nested mesh for every N): DistMG (distributed levels down
+    to 4 cells per rank, then an all-gathered replicated coarse cycle) + DistPCG (all-reduced dots), AVS 2+2 steps;
+    device time of the whole solve, max over ranks.  2D k: L = 11 (k=2,3) / 10; 3D: L = 7 (k <= 3) / 6."""
+    import torch
+    import torch.distributed as dist
+    from paper_2412_05082_b200 import api
+    from paper_2412_05082_b200.dist import DistMG, DistPCG
+    k, d = args.degree, args.dim
+    Lp = ({2: 11, 3: 11, 4: 10, 5: 9, 6: 9, 7: 9} if d == 2 else {2: 7, 3: 7, 4: 6, 5: 6})[k]
+    cp = api.Context(d, k, Lp, device=local)
+    b = cp.rhs(Lp)
+    mg = DistMG(cp, "avs", 2, 0.25 if d == 2 else 0.1, symmetric=True)
+    lev = mg.levels[Lp]
+    s = lev.slab
+    bw = b.view(-1, lev.row)[s.row0: s.row0 + s.lrows].reshape(-1).clone()
+    del b
+    solver = DistPCG(mg)
+    solver.solve(bw, max_iter=2)                         # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x, n, hist = solver.solve(bw)
+    e1.record()
+    torch.cuda.synchronize()
+    t = max_over_ranks(e0.elapsed_time(e1) * 1e-3, world)
+    out = {"seconds": round(t, 4), "iterations": n, "dofs": cp.n_dofs(Lp), "level": Lp,
+           "distributed_levels": sorted(mg.levels), "exchanges_per_solve": mg.exchanges,
+           "solved_gdofs": round(cp.n_dofs(Lp) / t / 1e9, 4),
+           "config": f"{d}D Q{k}, L={Lp}, AVS 2+2 steps, CG rtol 1e-8, FP64, {world} slabs"}
+    cp.close()
+    return out
 
 
 def traffic_from_profiles(kernel_key):
