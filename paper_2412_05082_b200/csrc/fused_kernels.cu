@@ -1200,8 +1200,6 @@ bool fused_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega,
                      int64_t* launches) {
   if (F.d != 2) return false;
   if (count == 0) return true;
-  static const int split = std::getenv("C0IP_MVS_SPLIT") ? std::atoi(std::getenv("C0IP_MVS_SPLIT")) : 0;
-  if (split == 1) return false;                 // measurement knob: residual kernel + patch solves per colour
   if constexpr (std::is_same<T, double>::value) {
     if (mma_mvs2d(F, list, count, double(omega), b, x, st)) {
       (*launches)++;
