@@ -72,31 +72,40 @@ def face_vectors_1d(k, h):
     }
 
 
-def global_matrices_1d(k, N, sigma, eliminate=True, nq=None, bfac=BOUNDARY_PENALTY):
+def global_matrices_1d(k, N, sigma, eliminate=True, nq=None, bfac=BOUNDARY_PENALTY, nodes=None):
     """Global 1D M, L, B (scipy CSR).  Size (kN+1)^2, or (kN-1)^2 after elimination.
 
-    bfac: boundary-facet penalty factor (reading Q27; bfac=1 is SURVEY.md Appendix A)."""
-    h = 1.0 / N
-    Mc, Lc, Bc = element_matrices_1d(k, h, nq)
-    fv = face_vectors_1d(k, h)
+    bfac: boundary-facet penalty factor (reading Q27; bfac=1 is SURVEY.md Appendix A).
+    nodes: optional cell boundaries x_0 = 0 < x_1 < ... < x_N = 1 of a graded mesh (PAPER.md:73,
+    131): cell c has width h_c = x_{c+1} - x_c, the interior facet between cells c-1 and c uses the harmonic mean
+    h_f = 2 h_{c-1} h_c / (h_{c-1} + h_c) of the adjacent widths, a boundary facet h_f = h_c / bfac
+    (reading Q27).  Default: uniform, h = 1/N."""
+    hs = np.full(N, 1.0 / N) if nodes is None else np.diff(np.asarray(nodes, dtype=np.float64))
+    assert len(hs) == N and np.all(hs > 0)
     nn = k * N + 1
     rows, cols, vm, vl, vb = [], [], [], [], []
     loc = np.arange(k + 1)
     for c in range(N):
+        Mc, Lc, Bc = element_matrices_1d(k, hs[c], nq)
         g = c * k + loc
         rr, cc = np.meshgrid(g, g, indexing="ij")
         rows.append(rr.ravel()); cols.append(cc.ravel())
         vm.append(Mc.ravel()); vl.append(Lc.ravel()); vb.append(Bc.ravel())
     zeros = lambda n: np.zeros(n)
     for f in range(N + 1):
-        s_f = sigma
         if f == 0:
-            a, b = fv["lower"]; g = loc; s_f = bfac * sigma
+            a, b = face_vectors_1d(k, hs[0])["lower"]; g = loc; h_f = hs[0] / bfac
         elif f == N:
-            a, b = fv["upper"]; g = (N - 1) * k + loc; s_f = bfac * sigma
+            a, b = face_vectors_1d(k, hs[N - 1])["upper"]; g = (N - 1) * k + loc; h_f = hs[N - 1] / bfac
         else:
-            a, b = fv["interior"]; g = (f - 1) * k + np.arange(2 * k + 1)
-        F = (s_f / h) * np.outer(a, a) - np.outer(a, b) - np.outer(b, a)
+            fl, fr = face_vectors_1d(k, hs[f - 1]), face_vectors_1d(k, hs[f])
+            # jump / mean across the facet with the two cells' own scalings (PAPER.md:87-97)
+            a = np.zeros(2 * k + 1); b = np.zeros(2 * k + 1)
+            a[: k + 1] += fl["upper"][0]; b[: k + 1] += 0.5 * fl["upper"][1]
+            a[k:] += fr["lower"][0]; b[k:] += 0.5 * fr["lower"][1]
+            g = (f - 1) * k + np.arange(2 * k + 1)
+            h_f = 2.0 * hs[f - 1] * hs[f] / (hs[f - 1] + hs[f])
+        F = (sigma / h_f) * np.outer(a, a) - np.outer(a, b) - np.outer(b, a)
         rr, cc = np.meshgrid(g, g, indexing="ij")
         rows.append(rr.ravel()); cols.append(cc.ravel())
         vm.append(zeros(F.size)); vl.append(zeros(F.size)); vb.append(F.ravel())
@@ -107,6 +116,13 @@ def global_matrices_1d(k, N, sigma, eliminate=True, nq=None, bfac=BOUNDARY_PENAL
         keep = np.arange(1, nn - 1)
         M, L, B = (X[keep][:, keep].tocsr() for X in (M, L, B))
     return M, L, B
+
+
+def graded_nodes(N, beta=0.0):
+    """Cell boundaries of a graded 1D mesh on [0,1]: x_c = phi(c/N), phi(t) = t + beta t (1 - t) (|beta| < 1,
+    monotone); nested: the boundaries of the N/2-cell mesh are every second one."""
+    t = np.arange(N + 1) / N
+    return t + beta * t * (1.0 - t)
 
 
 def patch_range_1d(k, v):

@@ -37,18 +37,23 @@ def default_omega(d, kind, exact=False):
     return 0.8 if d == 2 else 0.7
 
 
-def embedding_1d(k, Nc):
-    """E (n_f x n_c): coarse global basis (Nc cells) evaluated at the fine (2Nc) interior nodes."""
+def embedding_1d(k, Nc, nodes_f=None):
+    """E (n_f x n_c): coarse global basis (Nc cells) evaluated at the fine (2Nc) interior nodes.
+    nodes_f: optional cell boundaries of the fine graded mesh (2Nc + 1 values); the coarse mesh is every second
+    boundary (nested refinement)."""
     Nf = 2 * Nc
     t = gauss_lobatto_points(k)
     bas = Basis1D(k)
     nf, nc = k * Nf - 1, k * Nc - 1
+    Xf = np.arange(Nf + 1) / Nf if nodes_f is None else np.asarray(nodes_f, dtype=np.float64)
+    Xc = Xf[::2]
     E = np.zeros((nf, nc))
     for i in range(nf):
         j = i + 1
-        x = (j // k + t[j % k]) / Nf
-        c = min(int(np.floor(x * Nc)), Nc - 1)
-        tl = x * Nc - c
+        cf = min(j // k, Nf - 1)
+        x = Xf[cf] + t[j - cf * k] * (Xf[cf + 1] - Xf[cf])
+        c = cf // 2
+        tl = (x - Xc[c]) / (Xc[c + 1] - Xc[c])
         vals = bas.eval(tl, 0)[:, 0]
         for m in range(k + 1):
             jc = c * k + m
@@ -58,26 +63,30 @@ def embedding_1d(k, Nc):
     return E
 
 
-def prolongation(k, d, Nc):
-    E = sp.csr_matrix(embedding_1d(k, Nc))
-    P = E
-    for _ in range(d - 1):
-        P = sp.kron(E, P)          # kron(E_y, E_x) etc.: x fastest
+def prolongation(k, d, Nc, nodes_f=None):
+    """P = kron(E_{d-1}, ..., E_0) (x fastest); nodes_f: per-axis fine cell boundaries of a graded mesh."""
+    Es = [sp.csr_matrix(embedding_1d(k, Nc, None if nodes_f is None else nodes_f[a])) for a in range(d)]
+    P = Es[0]
+    for a in range(1, d):
+        P = sp.kron(Es[a], P)      # kron(E_y, E_x) etc.: x fastest
     return P.tocsr()
 
 
 class Hierarchy:
     """Levels 1..L (N = 2^l, reading Q9) with A_l, patch solvers and P_l (coarse l-1 -> l)."""
 
-    def __init__(self, k, d, L, sigma, dtype=np.float64):
+    def __init__(self, k, d, L, sigma, dtype=np.float64, nodes=None):
+        """nodes: optional per-axis cell boundaries of the finest level (graded mesh); level l uses
+        every 2^(L-l)-th boundary."""
         self.k, self.d, self.L, self.sigma = k, d, L, sigma
         self.A, self.ps, self.P = {}, {}, {}
         for l in range(1, L + 1):
             N = level_cells(l)
-            self.A[l] = assemble(k, d, N, sigma)
-            self.ps[l] = PatchSolvers(k, d, N, sigma)
+            nl = None if nodes is None else [np.asarray(x)[:: 2 ** (L - l)] for x in nodes]
+            self.A[l] = assemble(k, d, N, sigma, nodes=nl)
+            self.ps[l] = PatchSolvers(k, d, N, sigma, nodes=nl)
             if l > 1:
-                self.P[l] = prolongation(k, d, level_cells(l - 1))
+                self.P[l] = prolongation(k, d, level_cells(l - 1), nodes_f=nl)
         self.set_dtype(dtype)
 
     def set_dtype(self, dtype):

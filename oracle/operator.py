@@ -31,24 +31,59 @@ def _tensor(tables):
 
 
 def reference_cell_matrix(k, d, h, nq=None):
-    """(k+1)^d square matrix of sum_{a,b} int_K d_ab u d_ab v on a cube cell of width h."""
+    """(k+1)^d square matrix of sum_{a,b} int_K d_ab u d_ab v on a box cell of widths h (scalar: a cube;
+    sequence: per-axis widths of a graded / anisotropic cell)."""
+    hs = np.broadcast_to(np.asarray(h, dtype=np.float64), (d,))
     bas = Basis1D(k)
     nq = nq or (k + 2)
     t, w = gauss_legendre(nq)
-    V, D1, D2 = bas.eval(t, 0), bas.eval(t, 1) / h, bas.eval(t, 2) / h ** 2
-    W = _tensor([w[None, :]] * d).ravel() * h ** d
+    V, D1r, D2r = bas.eval(t, 0), bas.eval(t, 1), bas.eval(t, 2)
+    W = _tensor([w[None, :]] * d).ravel() * np.prod(hs)
     K = 0.0
     for a in range(d):
         for b in range(d):
             tabs = []
             for ax in range(d):
                 if a == b:
-                    tabs.append(D2 if ax == a else V)
+                    tabs.append(D2r / hs[ax] ** 2 if ax == a else V)
                 else:
-                    tabs.append(D1 if ax in (a, b) else V)
+                    tabs.append(D1r / hs[ax] if ax in (a, b) else V)
             H = _tensor(tabs)                      # [nl, Q]: d_ab phi_m at points
             K = K + (H * W) @ H.T
     return K
+
+
+def graded_face_matrix(k, d, axis, kind, sigma, ht, hm, hp=None, nq=None, bfac=BOUNDARY_PENALTY):
+    """Face matrix of a facet perpendicular to `axis` on a graded Cartesian mesh: ht = the d
+    widths of the facet's cells (only the tangential ones are used), hm / hp = the normal widths of the lower /
+    upper cell; h_e = harmonic mean 2 hm hp / (hm + hp) on an interior facet, h / bfac on a
+    boundary facet (reading Q27).  kind as in reference_face_matrix."""
+    bas = Basis1D(k)
+    nq = nq or (k + 2)
+    t, w = gauss_legendre(nq)
+    V = bas.eval(t, 0)
+    ht = np.asarray(ht, dtype=np.float64)
+    tang = [ax for ax in range(d) if ax != axis]
+    Wf = _tensor([w[None, :]] * (d - 1)).ravel() * np.prod(ht[tang]) if d > 1 else np.ones(1)
+
+    def trace(tn, der, hn):
+        tabs = [V] * d
+        tabs = list(tabs)
+        tabs[axis] = bas.eval(tn, der) / hn ** der
+        return _tensor(tabs)
+
+    if kind == "interior":
+        J = np.vstack([trace(1.0, 1, hm), -trace(0.0, 1, hp)])
+        Mn = np.vstack([0.5 * trace(1.0, 2, hm), 0.5 * trace(0.0, 2, hp)])
+        he = 2.0 * hm * hp / (hm + hp)
+    elif kind == "lower":
+        J, Mn, he = -trace(0.0, 1, hm), trace(0.0, 2, hm), hm / bfac
+    elif kind == "upper":
+        J, Mn, he = trace(1.0, 1, hm), trace(1.0, 2, hm), hm / bfac
+    else:
+        raise ValueError(kind)
+    JW, MW = J * Wf, Mn * Wf
+    return (sigma / he) * (JW @ J.T) - JW @ Mn.T - MW @ J.T
 
 
 def reference_face_matrix(k, d, h, axis, kind, sigma, nq=None, bfac=BOUNDARY_PENALTY):
@@ -97,12 +132,16 @@ def _local_full_ids(k, d, N, cells):
     return (j * strides).sum(-1)
 
 
-def assemble_full(k, d, N, sigma, cells=None, bfac=BOUNDARY_PENALTY):
+def assemble_full(k, d, N, sigma, cells=None, bfac=BOUNDARY_PENALTY, nodes=None):
     """COO->CSR of the C0IP form over full nodes (boundary nodes included).
 
     cells: optional [m, d] int array of included cells (a window); all faces whose adjacent
     cells are all included are added.  Default: every cell (the global matrix).
+    nodes: optional list of d arrays of cell boundaries (graded / anisotropic Cartesian mesh):
+    every cell and facet matrix is then integrated with its own widths (graded_face_matrix).
     """
+    if nodes is not None:
+        return _assemble_full_graded(k, d, N, sigma, bfac, [np.asarray(x, dtype=np.float64) for x in nodes])
     h = 1.0 / N
     nn = k * N + 1
     if cells is None:
@@ -140,6 +179,39 @@ def assemble_full(k, d, N, sigma, cells=None, bfac=BOUNDARY_PENALTY):
     return sp.csr_matrix((vals, (rows, cols)), shape=(nn ** d, nn ** d))
 
 
+def _assemble_full_graded(k, d, N, sigma, bfac, nodes):
+    nn = k * N + 1
+    hs = [np.diff(x) for x in nodes]
+    cells = np.array(list(itertools.product(range(N), repeat=d)))[:, ::-1]
+    rows, cols, vals = [], [], []
+    cache = {}
+
+    def add(ids, Mat):
+        rows.append(np.repeat(ids, Mat.shape[1], axis=1).ravel())
+        cols.append(np.tile(ids, (1, Mat.shape[0])).ravel())
+        vals.append(np.broadcast_to(Mat.ravel(), (ids.shape[0], Mat.size)).ravel())
+
+    for c in cells:
+        hc = tuple(hs[a][c[a]] for a in range(d))
+        key = ("cell", hc)
+        if key not in cache:
+            cache[key] = reference_cell_matrix(k, d, hc)
+        add(_local_full_ids(k, d, N, c[None, :]), cache[key])
+        for a in range(d):
+            if c[a] == 0:
+                add(_local_full_ids(k, d, N, c[None, :]),
+                    graded_face_matrix(k, d, a, "lower", sigma, hc, hc[a], bfac=bfac))
+            if c[a] == N - 1:
+                add(_local_full_ids(k, d, N, c[None, :]),
+                    graded_face_matrix(k, d, a, "upper", sigma, hc, hc[a], bfac=bfac))
+            else:
+                nb = c.copy(); nb[a] += 1
+                Fi = graded_face_matrix(k, d, a, "interior", sigma, hc, hc[a], hs[a][c[a] + 1], bfac=bfac)
+                add(np.hstack([_local_full_ids(k, d, N, c[None, :]), _local_full_ids(k, d, N, nb[None, :])]), Fi)
+    rows = np.concatenate(rows); cols = np.concatenate(cols); vals = np.concatenate(vals)
+    return sp.csr_matrix((vals, (rows, cols)), shape=(nn ** d, nn ** d))
+
+
 def interior_full_ids(k, d, N):
     """Full-node ids of the interior nodes, in interior (i) order, x fastest."""
     nn = k * N + 1
@@ -153,29 +225,32 @@ def interior_full_ids(k, d, N):
     return idx.ravel()
 
 
-def assemble(k, d, N, sigma, bfac=BOUNDARY_PENALTY):
-    """A_ell over interior DoFs (CSR), boundary rows/cols eliminated (reading Q26)."""
-    Af = assemble_full(k, d, N, sigma, bfac=bfac)
+def assemble(k, d, N, sigma, bfac=BOUNDARY_PENALTY, nodes=None):
+    """A_ell over interior DoFs (CSR), boundary rows/cols eliminated (reading Q26); nodes: graded mesh."""
+    Af = assemble_full(k, d, N, sigma, bfac=bfac, nodes=nodes)
     keep = interior_full_ids(k, d, N)
     return Af[keep][:, keep].tocsr()
 
 
-def rhs_load(k, d, N, f, nq=None):
+def rhs_load(k, d, N, f, nq=None, nodes=None):
     """b_i = int f phi_i (Eq. bfandrhs) by tensor Gauss quadrature per cell.
 
     f(*coords) takes d arrays of physical coordinates.  nq defaults to k+3.
+    nodes: optional per-axis cell boundaries (graded mesh).
     """
-    h = 1.0 / N
+    nodes = [np.arange(N + 1) / N] * d if nodes is None else [np.asarray(x, dtype=np.float64) for x in nodes]
+    hs = [np.diff(x) for x in nodes]
     nq = nq or (k + 3)
     bas = Basis1D(k)
     t, w = gauss_legendre(nq)
     Phi = _tensor([bas.eval(t, 0)] * d)                      # [nl, Q]
-    W = _tensor([w[None, :]] * d).ravel() * h ** d
+    W0 = _tensor([w[None, :]] * d).ravel()
     cells = np.array(list(itertools.product(range(N), repeat=d)))[:, ::-1]
     tq = np.array(list(itertools.product(range(nq), repeat=d)))[:, ::-1]   # x fastest points
-    coords = [(cells[:, a][:, None] + t[tq[:, a]][None, :]) * h for a in range(d)]
+    coords = [nodes[a][cells[:, a]][:, None] + t[tq[:, a]][None, :] * hs[a][cells[:, a]][:, None] for a in range(d)]
+    vol = np.prod([hs[a][cells[:, a]] for a in range(d)], axis=0)            # [ncells]
     fv = f(*coords)                                          # [ncells, Q]
-    contrib = (fv * W) @ Phi.T                               # [ncells, nl]
+    contrib = (fv * W0[None, :] * vol[:, None]) @ Phi.T      # [ncells, nl]
     nn = k * N + 1
     bf = np.zeros(nn ** d)
     np.add.at(bf, _local_full_ids(k, d, N, cells).ravel(), contrib.ravel())
@@ -202,7 +277,7 @@ def paper_solution(d):
     return u
 
 
-def boundary_data_load(k, d, N, sigma, nq=None, bfac=BOUNDARY_PENALTY):
+def boundary_data_load(k, d, N, sigma, nq=None, bfac=BOUNDARY_PENALTY, nodes=None):
     """Nitsche boundary-data part of F for d_n u = g on the boundary (reading Q8b).
 
     PAPER.md:488 fixes u* = prod sin(pi x_a) as the solution; u* = 0 on the boundary but its
@@ -214,12 +289,13 @@ def boundary_data_load(k, d, N, sigma, nq=None, bfac=BOUNDARY_PENALTY):
     (normal +e_a): g = d_n u* = -pi prod_{b != a} sin(pi x_b).  Facet quadrature: k+3 Gauss points
     per cell and tangential axis.
     """
-    h = 1.0 / N
+    nodes = [np.arange(N + 1) / N] * d if nodes is None else [np.asarray(x, dtype=np.float64) for x in nodes]
+    hs = [np.diff(x) for x in nodes]
     nq = nq or (k + 3)
     bas = Basis1D(k)
     t, w = gauss_legendre(nq)
     V = bas.eval(t, 0)
-    Wf = _tensor([w[None, :]] * (d - 1)).ravel() * h ** (d - 1) if d > 1 else np.ones(1)
+    Wf0 = _tensor([w[None, :]] * (d - 1)).ravel() if d > 1 else np.ones(1)
     tq = np.array(list(itertools.product(range(nq), repeat=d - 1)))[:, ::-1] if d > 1 else np.zeros((1, 0), int)
     nn = k * N + 1
     bf = np.zeros(nn ** d)
@@ -227,25 +303,39 @@ def boundary_data_load(k, d, N, sigma, nq=None, bfac=BOUNDARY_PENALTY):
         for side in (0, 1):
             tn = float(side)
             sgn = 1.0 if side == 1 else -1.0
+            hn = hs[a][0 if side == 0 else N - 1]                  # normal width of the boundary cells
             # traces on the facet: [nl, Qf] for d_n phi and d_n^2 phi (x fastest over the cell's dofs)
-            tabs1 = [V] * d; tabs1[a] = sgn * bas.eval(tn, 1) / h
-            tabs2 = [V] * d; tabs2[a] = bas.eval(tn, 2) / h ** 2
+            tabs1 = [V] * d; tabs1[a] = sgn * bas.eval(tn, 1) / hn
+            tabs2 = [V] * d; tabs2[a] = bas.eval(tn, 2) / hn ** 2
             Dn1, Dn2 = _tensor(tabs1), _tensor(tabs2)
             cells = np.array(list(itertools.product(range(N), repeat=d)))[:, ::-1]
             cells = cells[cells[:, a] == (0 if side == 0 else N - 1)]
             others = [b for b in range(d) if b != a]
-            g = -np.pi * np.ones((len(cells), len(Wf)))
+            g = -np.pi * np.ones((len(cells), len(Wf0)))
+            area = np.ones(len(cells))
             for j, b in enumerate(others):
-                g = g * np.sin(np.pi * (cells[:, b][:, None] + t[tq[:, j]][None, :]) * h)
-            contrib = (g * Wf) @ ((bfac * sigma / h) * Dn1 - Dn2).T        # [ncells, nl]
+                hb = hs[b][cells[:, b]]
+                g = g * np.sin(np.pi * (nodes[b][cells[:, b]][:, None] + t[tq[:, j]][None, :] * hb[:, None]))
+                area = area * hb
+            contrib = (g * Wf0[None, :] * area[:, None]) @ ((bfac * sigma / hn) * Dn1 - Dn2).T   # [ncells, nl]
             np.add.at(bf, _local_full_ids(k, d, N, cells).ravel(), contrib.ravel())
     return bf[interior_full_ids(k, d, N)]
 
 
-def paper_rhs(k, d, N, sigma, bfac=BOUNDARY_PENALTY):
+def paper_rhs(k, d, N, sigma, bfac=BOUNDARY_PENALTY, nodes=None):
     """F of the solve experiments: int f v with f = Delta^2 u* plus the
     boundary-data terms of boundary_data_load, so that u_h -> u* = prod sin(pi x_a)."""
-    return rhs_load(k, d, N, paper_load(d)) + boundary_data_load(k, d, N, sigma, bfac=bfac)
+    return (rhs_load(k, d, N, paper_load(d), nodes=nodes) +
+            boundary_data_load(k, d, N, sigma, bfac=bfac, nodes=nodes))
+
+
+def dof_coords_graded(k, X):
+    """Physical coordinates of the interior 1D DoFs of the graded mesh with cell boundaries X."""
+    from .basis import gauss_lobatto_points
+    X = np.asarray(X, dtype=np.float64)
+    t = gauss_lobatto_points(k)
+    N = len(X) - 1
+    return np.array([X[c] + t[m] * (X[c + 1] - X[c]) for c in range(N) for m in range(k)][1:])
 
 
 def dof_coords(k, N, i):

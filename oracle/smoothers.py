@@ -31,19 +31,25 @@ def _kron_all(mats):
 class PatchSolvers:
     """Dense Cholesky factors of A~_v per variant tuple, plus the patch DoF maps."""
 
-    def __init__(self, k, d, N, sigma, exact_A=None):
+    def __init__(self, k, d, N, sigma, exact_A=None, nodes=None):
+        """nodes: optional per-axis cell boundaries (graded mesh): the 1D matrices are per axis and
+        every patch has its own blocks (group key = vertex tuple instead of the axis-variant tuple)."""
         self.k, self.d, self.N = k, d, N
-        M, L, B = (X.toarray() for X in global_matrices_1d(k, N, sigma))
+        mats = [[X.toarray() for X in global_matrices_1d(k, N, sigma, nodes=None if nodes is None else nodes[a])]
+                for a in range(d)]
         self.verts = patch_vertices(d, N)
         self.dofs = all_patch_dofs(k, d, N)
         self.groups = {}          # variant tuple -> (patch ids, factor, dense matrix)
-        keys = [tuple(patch_variant(va, N) for va in v) for v in self.verts]
+        if nodes is None:
+            keys = [tuple(patch_variant(va, N) for va in v) for v in self.verts]
+        else:
+            keys = [tuple(int(va) for va in v) for v in self.verts]
         for key in sorted(set(keys)):
             ids = np.array([i for i, kk in enumerate(keys) if kk == key])
             v0 = self.verts[ids[0]]
             if exact_A is None:
-                Ms = [M[np.ix_(patch_range_1d(k, va), patch_range_1d(k, va))] for va in v0]
-                Bs = [B[np.ix_(patch_range_1d(k, va), patch_range_1d(k, va))] for va in v0]
+                Ms = [mats[a][0][np.ix_(patch_range_1d(k, va), patch_range_1d(k, va))] for a, va in enumerate(v0)]
+                Bs = [mats[a][2][np.ix_(patch_range_1d(k, va), patch_range_1d(k, va))] for a, va in enumerate(v0)]
                 At = 0.0
                 for a in range(d):
                     At = At + _kron_all([Bs[b] if b == a else Ms[b] for b in range(d)])
