@@ -80,6 +80,16 @@ typedef struct {
  * PAPER.md:134-142), OOM, CUDA.  *out is set only on success. */
 c0ip_status c0ip_create(const c0ip_config* cfg, c0ip_ctx* out);
 c0ip_status c0ip_destroy(c0ip_ctx ctx);
+
+/* As c0ip_create on a graded / anisotropic Cartesian mesh ("the discretization
+ * only requires shape regular, locally uniform cells"): nodes[a] (host, a < dim) holds the N+1 cell boundaries
+ * 0 = x_0 < ... < x_N = 1 of axis a on the finest level (N = 2^finest_level, or cells_override), NULL = uniform;
+ * level l uses every 2^(L-l)-th boundary (nested refinement).  Every cell has its own widths, an
+ * interior facet h_e = harmonic mean of the adjacent widths, a boundary facet h_e = h/2 (Q27); the
+ * FDM factors are per vertex (no translation invariance) and all operations use the generic per-axis kernels.
+ * c0ip_get_fdm and the exact local solver return STATE, the slab calls STATE (no fused level).  ARG for nodes that
+ * do not start at 0, end at 1 or increase strictly; the arrays are copied (not retained). */
+c0ip_status c0ip_create_graded(const c0ip_config* cfg, const double* const* nodes, c0ip_ctx* out);
 const char* c0ip_last_error(void);
 c0ip_status c0ip_set_path(c0ip_ctx ctx, c0ip_path path);
 

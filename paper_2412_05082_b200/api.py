@@ -57,12 +57,18 @@ class MG:
 
 
 class Context:
-    def __init__(self, dim, degree, finest_level, cells_override=0, penalty_scale=1.0, device=0):
+    def __init__(self, dim, degree, finest_level, cells_override=0, penalty_scale=1.0, device=0, nodes=None):
+        """nodes: optional per-axis cell boundaries of the finest level (graded mesh, c0ip_create_graded)."""
         self._lib = L.load()
         cfg = L.Config(int(dim), int(degree), int(finest_level), int(cells_override), float(penalty_scale),
                        int(device))
         h = C.c_void_p()
-        L.check(self._lib.c0ip_create(C.byref(cfg), C.byref(h)))
+        if nodes is None:
+            L.check(self._lib.c0ip_create(C.byref(cfg), C.byref(h)))
+        else:
+            self._nodes = [None if x is None else np.ascontiguousarray(x, dtype=np.float64) for x in nodes]
+            ptrs = (C.c_void_p * 3)(*[None if x is None else x.ctypes.data for x in self._nodes + [None] * (3 - len(self._nodes))])
+            L.check(self._lib.c0ip_create_graded(C.byref(cfg), ptrs, C.byref(h)))
         self.h = h
         self.dim, self.degree = int(dim), int(degree)
         self.finest_level = int(finest_level)

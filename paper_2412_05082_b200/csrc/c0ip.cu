@@ -79,6 +79,7 @@ struct Tables {
   DevArr<T> M, L, B;                  // square bands (scaled to h), n x (4k+1)
   DevArr<T> E, Et;                    // transfer bands (this level = fine)
   DevArr<T> S[4], lam[4];
+  DevArr<T> Ma[3], La[3], Ba[3], Ea[3], Eta[3], Sv[3], lamv[3];   // graded levels: per-axis tables (f4)
   // per-dtype workspaces
   DevArr<T> tmp[6];
   DevArr<T> sres;                     // smoother residual
@@ -125,6 +126,12 @@ struct Level {
   DevArr<int32_t> colors_d, parity_d;
   std::unique_ptr<c0ip::FusedLevel, c0ip::FusedLevelDeleter> fused;
   std::unique_ptr<ExactDev> exact;    // built on first use of the exact local solver
+  // graded / anisotropic Cartesian meshes: per-axis cell boundaries, bands, transfers
+  bool graded = false;
+  std::vector<double> nodes[3];
+  c0ip::Band Ma[3], La[3], Ba[3];
+  c0ip::RectBand Ea[3], Eta[3];
+  DevArr<int64_t> Ealo[3], Etalo[3];
 };
 
 }  // namespace
@@ -136,6 +143,8 @@ struct c0ip_ctx_s {
   int lmin = 1, lmax = 1;
   c0ip_path path = C0IP_PATH_AUTO;
   c0ip_local_solver local = C0IP_LOCAL_FDM;
+  bool graded = false;
+  std::vector<double> nodes[3];                    // finest-level cell boundaries per axis (graded meshes)
   std::map<std::tuple<int, int64_t, int64_t>, std::unique_ptr<WinLists>> wins;   // slab MVS patch lists
   c0ip::RefData ref;
   std::vector<Level> levels;          // index = level number (entries < lmin unused)
@@ -162,6 +171,13 @@ struct c0ip_ctx_s {
         t->free();
       for (int i = 0; i < 6; ++i) { L.t64.tmp[i].free(); L.t32.tmp[i].free(); }
       for (int i = 0; i < 4; ++i) { L.t64.S[i].free(); L.t64.lam[i].free(); L.t32.S[i].free(); L.t32.lam[i].free(); }
+      for (int a = 0; a < 3; ++a) {
+        for (auto* t : {&L.t64.Ma[a], &L.t64.La[a], &L.t64.Ba[a], &L.t64.Ea[a], &L.t64.Eta[a], &L.t64.Sv[a],
+                        &L.t64.lamv[a]}) t->free();
+        for (auto* t : {&L.t32.Ma[a], &L.t32.La[a], &L.t32.Ba[a], &L.t32.Ea[a], &L.t32.Eta[a], &L.t32.Sv[a],
+                        &L.t32.lamv[a]}) t->free();
+        L.Ealo[a].free(); L.Etalo[a].free();
+      }
       L.Elo.free(); L.Etlo.free(); L.colors_d.free(); L.parity_d.free();
       L.fused.reset();
       L.exact.reset();
@@ -271,14 +287,20 @@ void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStr
   if (jhi <= jlo) return;
   Tables<T>& t = tab<T>(L);
   ensure_tmp<T>(L, d);
-  auto Mo = square_op(t.M, k, n), Lo = square_op(t.L, k, n), Bo = square_op(t.B, k, n);
+  // per-axis operators (identical on uniform levels; graded levels have their own per axis)
+  c0ip::LineOp<T> Mx[3], Lx[3], Bx[3];
+  for (int a = 0; a < 3; ++a) {
+    Mx[a] = square_op(L.graded ? t.Ma[a] : t.M, k, n);
+    Lx[a] = square_op(L.graded ? t.La[a] : t.L, k, n);
+    Bx[a] = square_op(L.graded ? t.Ba[a] : t.B, k, n);
+  }
   const int64_t n2 = (d == 3) ? n : 1;
   const int sax = d - 1;                                         // slowest axis
   const int64_t tlo = std::max<int64_t>(0, jlo - 2 * k), thi = std::min<int64_t>(n, jhi + 2 * k);
   auto rows = [&](c0ip::AxisArgs<T>& a, int64_t lo, int64_t hi) { a.sax = sax; a.s0 = lo; a.scnt = hi - lo; };
   // x-stage: B_x x, L_x x, M_x x
   {
-    const c0ip::LineOp<T>* ops[3] = {&Bo, &Lo, &Mo};
+    const c0ip::LineOp<T>* ops[3] = {&Bx[0], &Lx[0], &Mx[0]};
     for (int i = 0; i < 3; ++i) {
       auto a = axis_args<T>(n, n, n2, 0, t.tmp[i].p);
       add_term(a, x, *ops[i], T(1));
@@ -290,9 +312,9 @@ void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStr
   if (d == 2) {
     // y = M_y (B_x x) + 2 L_y (L_x x) + B_y (M_x x)
     auto a = axis_args<T>(n, n, 1, 1, y);
-    add_term(a, (const T*)t.tmp[0].p, Mo, sg);
-    add_term(a, (const T*)t.tmp[1].p, Lo, T(2) * sg);
-    add_term(a, (const T*)t.tmp[2].p, Bo, sg);
+    add_term(a, (const T*)t.tmp[0].p, Mx[1], sg);
+    add_term(a, (const T*)t.tmp[1].p, Lx[1], T(2) * sg);
+    add_term(a, (const T*)t.tmp[2].p, Bx[1], sg);
     if (b) { a.z = b; a.gamma = T(1); }
     rows(a, jlo, jhi);
     launch_axis(ctx, a, st);
@@ -301,26 +323,26 @@ void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStr
   // y-stage: P = M_y B_x + B_y M_x + 2 L_y L_x ; Q = L_y M_x + M_y L_x ; R = M_y M_x
   {
     auto a = axis_args<T>(n, n, n, 1, t.tmp[3].p);
-    add_term(a, (const T*)t.tmp[0].p, Mo, T(1));
-    add_term(a, (const T*)t.tmp[2].p, Bo, T(1));
-    add_term(a, (const T*)t.tmp[1].p, Lo, T(2));
+    add_term(a, (const T*)t.tmp[0].p, Mx[1], T(1));
+    add_term(a, (const T*)t.tmp[2].p, Bx[1], T(1));
+    add_term(a, (const T*)t.tmp[1].p, Lx[1], T(2));
     rows(a, tlo, thi);
     launch_axis(ctx, a, st);
     auto q = axis_args<T>(n, n, n, 1, t.tmp[4].p);
-    add_term(q, (const T*)t.tmp[2].p, Lo, T(1));
-    add_term(q, (const T*)t.tmp[1].p, Mo, T(1));
+    add_term(q, (const T*)t.tmp[2].p, Lx[1], T(1));
+    add_term(q, (const T*)t.tmp[1].p, Mx[1], T(1));
     rows(q, tlo, thi);
     launch_axis(ctx, q, st);
     auto r = axis_args<T>(n, n, n, 1, t.tmp[5].p);
-    add_term(r, (const T*)t.tmp[2].p, Mo, T(1));
+    add_term(r, (const T*)t.tmp[2].p, Mx[1], T(1));
     rows(r, tlo, thi);
     launch_axis(ctx, r, st);
   }
   // z-stage: y = M_z P + 2 L_z Q + B_z R
   auto a = axis_args<T>(n, n, n, 2, y);
-  add_term(a, (const T*)t.tmp[3].p, Mo, sg);
-  add_term(a, (const T*)t.tmp[4].p, Lo, T(2) * sg);
-  add_term(a, (const T*)t.tmp[5].p, Bo, sg);
+  add_term(a, (const T*)t.tmp[3].p, Mx[2], sg);
+  add_term(a, (const T*)t.tmp[4].p, Lx[2], T(2) * sg);
+  add_term(a, (const T*)t.tmp[5].p, Bx[2], sg);
   if (b) { a.z = b; a.gamma = T(1); }
   rows(a, jlo, jhi);
   launch_axis(ctx, a, st);
@@ -344,6 +366,10 @@ void patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, const int32_
   a.d = ctx->d; a.k = ctx->k; a.np = 2 * ctx->k - 1;
   a.N = L.N; a.n = L.n;
   for (int v = 0; v < 4; ++v) { a.S[v] = t.S[v].p; a.lam[v] = t.lam[v].p; }
+  for (int ax = 0; ax < 3; ++ax) {
+    a.Sv[ax] = L.graded ? t.Sv[ax].p : nullptr;
+    a.lamv[ax] = L.graded ? t.lamv[ax].p : nullptr;
+  }
   a.r = r; a.x = x; a.omega = omega;
   a.list = list; a.count = count; a.atomic = atomic;
   const int nloc = ipow(a.np, a.d);
@@ -385,6 +411,7 @@ void disjoint_patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, con
 }
 
 ExactDev& exact_tables(c0ip_ctx ctx, Level& L) {
+  if (L.graded) throw std::runtime_error("the exact local solver needs a uniform mesh (variant-tuple tables)");
   if (!L.exact) {
     std::unique_ptr<ExactDev> e(new ExactDev());
     const int nc = 1 << (ctx->d + 1);
@@ -493,35 +520,53 @@ void smooth_impl(c0ip_ctx ctx, Level& L, c0ip_smoother sm, int steps, T omega, b
   }
 }
 
+// transfer bands of the pass along `axis` (per axis on graded levels)
+template <typename T>
+c0ip::LineOp<T> e_op(Level& F, int axis) {
+  Tables<T>& t = tab<T>(F);
+  c0ip::LineOp<T> E;
+  E.v = F.graded ? t.Ea[axis].p : t.E.p;
+  E.lo = F.graded ? F.Ealo[axis].p : F.Elo.p;
+  E.width = F.E.width; E.hw = 0; E.n_in = F.E.cols;
+  return E;
+}
+template <typename T>
+c0ip::LineOp<T> et_op(Level& F, int axis) {
+  Tables<T>& t = tab<T>(F);
+  c0ip::LineOp<T> Et;
+  Et.v = F.graded ? t.Eta[axis].p : t.Et.p;
+  Et.lo = F.graded ? F.Etalo[axis].p : F.Etlo.p;
+  Et.width = F.Et.width; Et.hw = 0; Et.n_in = F.n;
+  return Et;
+}
+
 // fine += P coarse  (P = E (x) E (x) E, natural embedding)
 template <typename T>
 void prolongate_add_impl(c0ip_ctx ctx, Level& F, const T* coarse, T* fine, cudaStream_t st) {
-  if (ctx->path == C0IP_PATH_AUTO && ctx->d == 2 &&
+  if (ctx->path == C0IP_PATH_AUTO && ctx->d == 2 && !F.graded &&
       c0ip::fused_transfer2d<T>(ctx->k, true, F.N / 2, coarse, fine, st, &ctx->launches))
     return;
   Tables<T>& t = tab<T>(F);
   ensure_tmp<T>(F, ctx->d);
   const int64_t nf = F.n, nc = F.E.cols;
-  c0ip::LineOp<T> E;
-  E.v = t.E.p; E.lo = F.Elo.p; E.width = F.E.width; E.hw = 0; E.n_in = nc;
   if (ctx->d == 2) {
     auto a = axis_args<T>(nf, nc, 1, 0, t.tmp[0].p);
-    add_term(a, coarse, E, T(1));
+    add_term(a, coarse, e_op<T>(F, 0), T(1));
     launch_axis(ctx, a, st);
     auto b = axis_args<T>(nf, nf, 1, 1, fine);
-    add_term(b, (const T*)t.tmp[0].p, E, T(1));
+    add_term(b, (const T*)t.tmp[0].p, e_op<T>(F, 1), T(1));
     b.beta = T(1);
     launch_axis(ctx, b, st);
     return;
   }
   auto a = axis_args<T>(nf, nc, nc, 0, t.tmp[0].p);
-  add_term(a, coarse, E, T(1));
+  add_term(a, coarse, e_op<T>(F, 0), T(1));
   launch_axis(ctx, a, st);
   auto b = axis_args<T>(nf, nf, nc, 1, t.tmp[1].p);
-  add_term(b, (const T*)t.tmp[0].p, E, T(1));
+  add_term(b, (const T*)t.tmp[0].p, e_op<T>(F, 1), T(1));
   launch_axis(ctx, b, st);
   auto c = axis_args<T>(nf, nf, nf, 2, fine);
-  add_term(c, (const T*)t.tmp[1].p, E, T(1));
+  add_term(c, (const T*)t.tmp[1].p, e_op<T>(F, 2), T(1));
   c.beta = T(1);
   launch_axis(ctx, c, st);
 }
@@ -529,31 +574,29 @@ void prolongate_add_impl(c0ip_ctx ctx, Level& F, const T* coarse, T* fine, cudaS
 // coarse = P^T fine (restriction = transpose of the embedding)
 template <typename T>
 void restrict_impl(c0ip_ctx ctx, Level& F, const T* fine, T* coarse, cudaStream_t st) {
-  if (ctx->path == C0IP_PATH_AUTO && ctx->d == 2 &&
+  if (ctx->path == C0IP_PATH_AUTO && ctx->d == 2 && !F.graded &&
       c0ip::fused_transfer2d<T>(ctx->k, false, F.N / 2, fine, coarse, st, &ctx->launches))
     return;
   Tables<T>& t = tab<T>(F);
   ensure_tmp<T>(F, ctx->d);
   const int64_t nf = F.n, nc = F.E.cols;
-  c0ip::LineOp<T> Et;
-  Et.v = t.Et.p; Et.lo = F.Etlo.p; Et.width = F.Et.width; Et.hw = 0; Et.n_in = nf;
   if (ctx->d == 2) {
     auto a = axis_args<T>(nc, nf, 1, 0, t.tmp[0].p);
-    add_term(a, fine, Et, T(1));
+    add_term(a, fine, et_op<T>(F, 0), T(1));
     launch_axis(ctx, a, st);
     auto b = axis_args<T>(nc, nc, 1, 1, coarse);
-    add_term(b, (const T*)t.tmp[0].p, Et, T(1));
+    add_term(b, (const T*)t.tmp[0].p, et_op<T>(F, 1), T(1));
     launch_axis(ctx, b, st);
     return;
   }
   auto a = axis_args<T>(nc, nf, nf, 0, t.tmp[0].p);
-  add_term(a, fine, Et, T(1));
+  add_term(a, fine, et_op<T>(F, 0), T(1));
   launch_axis(ctx, a, st);
   auto b = axis_args<T>(nc, nc, nf, 1, t.tmp[1].p);
-  add_term(b, (const T*)t.tmp[0].p, Et, T(1));
+  add_term(b, (const T*)t.tmp[0].p, et_op<T>(F, 1), T(1));
   launch_axis(ctx, b, st);
   auto c = axis_args<T>(nc, nc, nc, 2, coarse);
-  add_term(c, (const T*)t.tmp[1].p, Et, T(1));
+  add_term(c, (const T*)t.tmp[1].p, et_op<T>(F, 2), T(1));
   launch_axis(ctx, c, st);
 }
 
@@ -703,15 +746,40 @@ void build_level(c0ip_ctx ctx, int l, int64_t N) {
   L.ndofs = 1;
   L.npatch = 1;
   for (int a = 0; a < d; ++a) { L.ndofs *= L.n; L.npatch *= (N - 1); }
-  c0ip::global_bands(ctx->ref, N, L.M, L.L, L.B);
-  const double h = L.h;
-  for (auto& v : L.M.v) v *= h;                       // M = h Mhat
-  for (auto& v : L.L.v) v /= h;                       // L = Lhat / h
-  for (auto& v : L.B.v) v /= h * h * h;               // B = Bhat / h^3
-  if (!c0ip::band_is_spd(L.B))
-    throw std::runtime_error("coercivity: 1D C0IP matrix B is not positive definite (penalty too small)");
-  std::string err;
-  if (!c0ip::make_fdm(ctx->ref, N, L.M, L.L, L.B, L.fdm, err)) throw std::runtime_error("coercivity: " + err);
+  if (ctx->graded) {
+    // graded / anisotropic Cartesian mesh: per-axis bands and per-vertex FDM factors, generic
+    // per-axis kernels only (the fused tile kernels assume uniform coefficients)
+    L.graded = true;
+    const int64_t stride = (int64_t(1) << (ctx->lmax - l));
+    std::string err;
+    for (int a = 0; a < d; ++a) {
+      L.nodes[a].clear();
+      for (size_t i = 0; i < ctx->nodes[a].size(); i += size_t(stride)) L.nodes[a].push_back(ctx->nodes[a][i]);
+      c0ip::global_bands_graded(ctx->ref, L.nodes[a], L.Ma[a], L.La[a], L.Ba[a]);
+      if (!c0ip::band_is_spd(L.Ba[a]))
+        throw std::runtime_error("coercivity: 1D C0IP matrix B is not positive definite (penalty too small)");
+      std::vector<double> Sv, lv;
+      if (!c0ip::make_fdm_vertices(k, N, L.Ma[a], L.La[a], L.Ba[a], Sv, lv, err))
+        throw std::runtime_error("coercivity: " + err);
+      for (auto* t : {&L.t64.Ma[a], &L.t64.La[a], &L.t64.Ba[a]}) (void)t;
+      L.t64.Ma[a].upload(L.Ma[a].v); L.t64.La[a].upload(L.La[a].v); L.t64.Ba[a].upload(L.Ba[a].v);
+      L.t32.Ma[a].upload(cast_vec<float>(L.Ma[a].v)); L.t32.La[a].upload(cast_vec<float>(L.La[a].v));
+      L.t32.Ba[a].upload(cast_vec<float>(L.Ba[a].v));
+      L.t64.Sv[a].upload(Sv); L.t64.lamv[a].upload(lv);
+      L.t32.Sv[a].upload(cast_vec<float>(Sv)); L.t32.lamv[a].upload(cast_vec<float>(lv));
+    }
+    L.M = L.Ma[0]; L.L = L.La[0]; L.B = L.Ba[0];         // axis 0 (c0ip_get_matrices_1d)
+  } else {
+    c0ip::global_bands(ctx->ref, N, L.M, L.L, L.B);
+    const double h = L.h;
+    for (auto& v : L.M.v) v *= h;                       // M = h Mhat
+    for (auto& v : L.L.v) v /= h;                       // L = Lhat / h
+    for (auto& v : L.B.v) v /= h * h * h;               // B = Bhat / h^3
+    if (!c0ip::band_is_spd(L.B))
+      throw std::runtime_error("coercivity: 1D C0IP matrix B is not positive definite (penalty too small)");
+    std::string err;
+    if (!c0ip::make_fdm(ctx->ref, N, L.M, L.L, L.B, L.fdm, err)) throw std::runtime_error("coercivity: " + err);
+  }
   L.t64.M.upload(L.M.v); L.t64.L.upload(L.L.v); L.t64.B.upload(L.B.v);
   L.t32.M.upload(cast_vec<float>(L.M.v)); L.t32.L.upload(cast_vec<float>(L.L.v)); L.t32.B.upload(cast_vec<float>(L.B.v));
   for (int v = 0; v < 4; ++v) {
@@ -743,12 +811,22 @@ void build_level(c0ip_ctx ctx, int l, int64_t N) {
   }
   L.colors_d.upload(L.colors_h);
   L.parity_d.upload(L.parity_h);
-  L.fused = c0ip::make_fused_level_impl(d, k, N, ctx->ref, L.fdm, h);
+  if (!L.graded) L.fused = c0ip::make_fused_level_impl(d, k, N, ctx->ref, L.fdm, L.h);
 }
 
 void build_transfer(c0ip_ctx ctx, int l) {
   Level& L = ctx->levels[l];
-  L.E = c0ip::embedding(ctx->k, ctx->levels[l - 1].N);
+  if (L.graded) {                                      // per-axis embeddings of the nested graded meshes
+    for (int a = 0; a < ctx->d; ++a) {
+      L.Ea[a] = c0ip::embedding_graded(ctx->k, L.nodes[a]);
+      L.Eta[a] = c0ip::transpose(L.Ea[a]);
+      L.t64.Ea[a].upload(L.Ea[a].v); L.t32.Ea[a].upload(cast_vec<float>(L.Ea[a].v));
+      L.t64.Eta[a].upload(L.Eta[a].v); L.t32.Eta[a].upload(cast_vec<float>(L.Eta[a].v));
+      L.Ealo[a].upload(L.Ea[a].lo);
+      L.Etalo[a].upload(L.Eta[a].lo);
+    }
+  }
+  L.E = L.graded ? L.Ea[0] : c0ip::embedding(ctx->k, ctx->levels[l - 1].N);
   L.Et = c0ip::transpose(L.E);
   L.t64.E.upload(L.E.v); L.t32.E.upload(cast_vec<float>(L.E.v));
   L.t64.Et.upload(L.Et.v); L.t32.Et.upload(cast_vec<float>(L.Et.v));
@@ -763,7 +841,16 @@ extern "C" {
 
 const char* c0ip_last_error(void) { return g_err.c_str(); }
 
-c0ip_status c0ip_create(const c0ip_config* cfg, c0ip_ctx* out) {
+static c0ip_status create_impl(const c0ip_config* cfg, const double* const* nodes, c0ip_ctx* out);
+
+c0ip_status c0ip_create(const c0ip_config* cfg, c0ip_ctx* out) { return create_impl(cfg, nullptr, out); }
+
+c0ip_status c0ip_create_graded(const c0ip_config* cfg, const double* const* nodes, c0ip_ctx* out) {
+  if (!nodes) return fail(C0IP_ERR_ARG, "null nodes");
+  return create_impl(cfg, nodes, out);
+}
+
+static c0ip_status create_impl(const c0ip_config* cfg, const double* const* nodes, c0ip_ctx* out) {
   if (!cfg || !out) return fail(C0IP_ERR_ARG, "null argument");
   if (cfg->dim != 2 && cfg->dim != 3) return fail(C0IP_ERR_ARG, "dim must be 2 or 3");
   if (cfg->degree < 2 || cfg->degree > 7) return fail(C0IP_ERR_ARG, "degree must be in [2,7]");
@@ -783,6 +870,19 @@ c0ip_status c0ip_create(const c0ip_config* cfg, c0ip_ctx* out) {
   ctx->lmax = cfg->finest_level;
   ctx->lmin = cfg->cells_override > 0 ? cfg->finest_level : 1;
   ctx->levels.resize(ctx->lmax + 1);
+  if (nodes) {                                           // graded mesh: cell boundaries of the finest level
+    const int64_t NL = cfg->cells_override > 0 ? cfg->cells_override : (int64_t(1) << cfg->finest_level);
+    ctx->graded = true;
+    for (int a = 0; a < ctx->d; ++a) {
+      std::vector<double> X(NL + 1);
+      for (int64_t i = 0; i <= NL; ++i) X[i] = nodes[a] ? nodes[a][i] : double(i) / double(NL);
+      if (std::fabs(X[0]) > 1e-14 || std::fabs(X[NL] - 1.0) > 1e-14)
+        return fail(C0IP_ERR_ARG, "graded nodes must start at 0 and end at 1");
+      for (int64_t i = 0; i < NL; ++i)
+        if (!(X[i + 1] > X[i])) return fail(C0IP_ERR_ARG, "graded nodes must be strictly increasing");
+      ctx->nodes[a] = X;
+    }
+  }
   try {
     for (int l = ctx->lmin; l <= ctx->lmax; ++l)
       build_level(ctx.get(), l, cfg->cells_override > 0 ? cfg->cells_override : (int64_t(1) << l));
@@ -878,6 +978,7 @@ c0ip_status c0ip_color_patches(c0ip_ctx ctx, int32_t level, int32_t color, int64
 }
 
 c0ip_status c0ip_get_fdm(c0ip_ctx ctx, int32_t level, int32_t variant, double* S, double* lambda) {
+  if (ctx && ctx->graded) return fail(C0IP_ERR_STATE, "graded meshes have per-vertex FDM factors (no variants)");
   c0ip_status s = check_level(ctx, level);
   if (s) return s;
   if (variant < 0 || variant > 3) return fail(C0IP_ERR_ARG, "variant out of range");
@@ -911,19 +1012,23 @@ c0ip_status c0ip_rhs(c0ip_ctx ctx, int32_t level, double* b, void* stream) {
   ABI_TRY
   Level& L = ctx->levels[level];
   cudaStream_t st = (cudaStream_t)stream;
-  std::vector<double> f1 = c0ip::sine_load_1d(ctx->k, L.N);
-  std::vector<double> g1 = c0ip::boundary_normal_1d(ctx->ref, L.N);
-  DevArr<double> tmp, tmpg;
-  tmp.upload(f1);
-  tmpg.upload(g1);
+  DevArr<double> tmp[3], tmpg[3];
+  c0ip::LoadArgs la;
+  for (int a = 0; a < 3; ++a) {
+    const int aa = a < ctx->d ? a : 0;
+    tmp[a].upload(L.graded ? c0ip::sine_load_1d_graded(ctx->k, L.nodes[aa]) : c0ip::sine_load_1d(ctx->k, L.N));
+    tmpg[a].upload(L.graded ? c0ip::boundary_normal_1d_graded(ctx->ref, L.nodes[aa])
+                            : c0ip::boundary_normal_1d(ctx->ref, L.N));
+    la.f1[a] = tmp[a].p;
+    la.g1[a] = tmpg[a].p;
+  }
   const double c = double(ctx->d * ctx->d) * std::pow(M_PI, 4);   // f = d^2 pi^4 prod sin (Q1, Q8)
   const double cb = -M_PI;                                        // g = d_n u* = -pi prod_{b!=a} sin (Q8b)
-  c0ip::outer_load_kernel<<<grid_for(L.ndofs), 256, 0, st>>>(ctx->d, L.n, tmp.p, tmpg.p, c, cb, b);
+  c0ip::outer_load_kernel<<<grid_for(L.ndofs), 256, 0, st>>>(ctx->d, L.n, la, c, cb, b);
   ctx->launches++;
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
-  tmp.free();
-  tmpg.free();
+  for (int a = 0; a < 3; ++a) { tmp[a].free(); tmpg[a].free(); }
   return C0IP_OK;
   ABI_CATCH
 }
@@ -1360,29 +1465,27 @@ void slab_restrict_impl(c0ip_ctx ctx, Level& F, const T* fv, T* cv, int64_t ic_l
   const int64_t nf = F.n, nc = F.E.cols;
   const int width = F.Et.width;
   const int64_t fr_lo = F.Et.lo[ic_lo], fr_hi = F.Et.lo[ic_hi - 1] + width;
-  c0ip::LineOp<T> Et;
-  Et.v = t.Et.p; Et.lo = F.Etlo.p; Et.width = width; Et.hw = 0; Et.n_in = nf;
   if (ctx->d == 2) {
     auto a = axis_args<T>(nc, nf, 1, 0, t.tmp[0].p);
-    add_term(a, fv, Et, T(1));
+    add_term(a, fv, et_op<T>(F, 0), T(1));
     a.sax = 1; a.s0 = fr_lo; a.scnt = fr_hi - fr_lo;
     launch_axis(ctx, a, st);
     auto b = axis_args<T>(nc, nc, 1, 1, cv);
-    add_term(b, (const T*)t.tmp[0].p, Et, T(1));
+    add_term(b, (const T*)t.tmp[0].p, et_op<T>(F, 1), T(1));
     b.sax = 1; b.s0 = ic_lo; b.scnt = ic_hi - ic_lo;
     launch_axis(ctx, b, st);
     return;
   }
   auto a = axis_args<T>(nc, nf, nf, 0, t.tmp[0].p);
-  add_term(a, fv, Et, T(1));
+  add_term(a, fv, et_op<T>(F, 0), T(1));
   a.sax = 2; a.s0 = fr_lo; a.scnt = fr_hi - fr_lo;
   launch_axis(ctx, a, st);
   auto b = axis_args<T>(nc, nc, nf, 1, t.tmp[1].p);
-  add_term(b, (const T*)t.tmp[0].p, Et, T(1));
+  add_term(b, (const T*)t.tmp[0].p, et_op<T>(F, 1), T(1));
   b.sax = 2; b.s0 = fr_lo; b.scnt = fr_hi - fr_lo;
   launch_axis(ctx, b, st);
   auto c = axis_args<T>(nc, nc, nc, 2, cv);
-  add_term(c, (const T*)t.tmp[1].p, Et, T(1));
+  add_term(c, (const T*)t.tmp[1].p, et_op<T>(F, 2), T(1));
   c.sax = 2; c.s0 = ic_lo; c.scnt = ic_hi - ic_lo;
   launch_axis(ctx, c, st);
 }
@@ -1395,30 +1498,28 @@ void slab_prolongate_impl(c0ip_ctx ctx, Level& F, const T* cv, T* fv, int64_t if
   const int64_t nf = F.n, nc = F.E.cols;
   const int width = F.E.width;
   const int64_t cr_lo = F.E.lo[if_lo], cr_hi = F.E.lo[if_hi - 1] + width;
-  c0ip::LineOp<T> E;
-  E.v = t.E.p; E.lo = F.Elo.p; E.width = width; E.hw = 0; E.n_in = nc;
   if (ctx->d == 2) {
     auto a = axis_args<T>(nf, nc, 1, 0, t.tmp[0].p);
-    add_term(a, cv, E, T(1));
+    add_term(a, cv, e_op<T>(F, 0), T(1));
     a.sax = 1; a.s0 = cr_lo; a.scnt = cr_hi - cr_lo;
     launch_axis(ctx, a, st);
     auto b = axis_args<T>(nf, nf, 1, 1, fv);
-    add_term(b, (const T*)t.tmp[0].p, E, T(1));
+    add_term(b, (const T*)t.tmp[0].p, e_op<T>(F, 1), T(1));
     b.beta = T(1);
     b.sax = 1; b.s0 = if_lo; b.scnt = if_hi - if_lo;
     launch_axis(ctx, b, st);
     return;
   }
   auto a = axis_args<T>(nf, nc, nc, 0, t.tmp[0].p);
-  add_term(a, cv, E, T(1));
+  add_term(a, cv, e_op<T>(F, 0), T(1));
   a.sax = 2; a.s0 = cr_lo; a.scnt = cr_hi - cr_lo;
   launch_axis(ctx, a, st);
   auto b = axis_args<T>(nf, nf, nc, 1, t.tmp[1].p);
-  add_term(b, (const T*)t.tmp[0].p, E, T(1));
+  add_term(b, (const T*)t.tmp[0].p, e_op<T>(F, 1), T(1));
   b.sax = 2; b.s0 = cr_lo; b.scnt = cr_hi - cr_lo;
   launch_axis(ctx, b, st);
   auto c = axis_args<T>(nf, nf, nf, 2, fv);
-  add_term(c, (const T*)t.tmp[1].p, E, T(1));
+  add_term(c, (const T*)t.tmp[1].p, e_op<T>(F, 2), T(1));
   c.beta = T(1);
   c.sax = 2; c.s0 = if_lo; c.scnt = if_hi - if_lo;
   launch_axis(ctx, c, st);

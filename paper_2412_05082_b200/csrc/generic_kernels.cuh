@@ -86,6 +86,8 @@ struct PatchArgs {
   int64_t N, n;           // cells, 1D interior dofs
   const T* S[4];          // per axis variant: S[l*np + i]  (np x np)
   const T* lam[4];
+  const T* Sv[3];         // graded meshes: per axis, per vertex v: Sv[a][(v-1) np^2 + l np + i]
+  const T* lamv[3];       //   and lamv[a][(v-1) np + i]; nullptr: the variant tables above
   const T* r;             // residual (global)
   T* x;                   // updated: x[g] += omega * u
   T omega;
@@ -149,7 +151,8 @@ __global__ void __launch_bounds__(256) patch_fdm_kernel(PatchArgs<T> a) {
       int64_t pid = patch_id(pp);
       T s = 0;
       if (pid >= 0) {
-        const T* S = a.S[axis_variant(vert(pid, ax), a.N)];
+        const int64_t vv = vert(pid, ax);
+        const T* S = a.Sv[ax] ? a.Sv[ax] + (vv - 1) * np * np : a.S[axis_variant(vv, a.N)];
         int li = (l / st) % np;
         int base = pp * nloc + l - li * st;
         for (int m = 0; m < np; ++m) s += S[m * np + li] * buf0[base + m * st];
@@ -167,7 +170,8 @@ __global__ void __launch_bounds__(256) patch_fdm_kernel(PatchArgs<T> a) {
     T den = 0;
     int ll = l;
     for (int ax = 0; ax < a.d; ++ax) {
-      den += a.lam[axis_variant(vert(pid, ax), a.N)][ll % np];
+      const int64_t vv = vert(pid, ax);
+      den += a.lamv[ax] ? a.lamv[ax][(vv - 1) * np + ll % np] : a.lam[axis_variant(vv, a.N)][ll % np];
       ll /= np;
     }
     buf0[it] = buf0[it] / den;
@@ -182,7 +186,8 @@ __global__ void __launch_bounds__(256) patch_fdm_kernel(PatchArgs<T> a) {
       int64_t pid = patch_id(pp);
       T s = 0;
       if (pid >= 0) {
-        const T* S = a.S[axis_variant(vert(pid, ax), a.N)];
+        const int64_t vv = vert(pid, ax);
+        const T* S = a.Sv[ax] ? a.Sv[ax] + (vv - 1) * np * np : a.S[axis_variant(vv, a.N)];
         int li = (l / st) % np;
         int base = pp * nloc + l - li * st;
         for (int m = 0; m < np; ++m) s += S[li * np + m] * buf0[base + m * st];
@@ -266,15 +271,19 @@ __global__ void __launch_bounds__(256) dot_final_kernel(int nparts, const double
 
 // b[g] = c * prod_a f1[i_a] + cb * sum_a g1[i_a] prod_{b != a} f1[i_b]
 // (separable paper load plus the separable Nitsche boundary data, reading Q8b)
-__global__ void outer_load_kernel(int d, int64_t n, const double* f1, const double* g1, double c,
-                                  double cb, double* b) {
+// (per-axis 1D factors f1[a], g1[a]: graded meshes have different ones per axis)
+struct LoadArgs {
+  const double* f1[3];
+  const double* g1[3];
+};
+__global__ void outer_load_kernel(int d, int64_t n, LoadArgs la, double c, double cb, double* b) {
   int64_t total = n * n * (d == 3 ? n : 1);
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
     int64_t i0 = g % n, i1 = (g / n) % n, i2 = g / (n * n);
-    const double f0 = f1[i0], fy = f1[i1], fz = d == 3 ? f1[i2] : 1.0;
+    const double f0 = la.f1[0][i0], fy = la.f1[1][i1], fz = d == 3 ? la.f1[2][i2] : 1.0;
     double v = c * f0 * fy * fz;
-    double w = g1[i0] * fy * fz + f0 * g1[i1] * fz;
-    if (d == 3) w += f0 * fy * g1[i2];
+    double w = la.g1[0][i0] * fy * fz + f0 * la.g1[1][i1] * fz;
+    if (d == 3) w += f0 * fy * la.g1[2][i2];
     b[g] = v + cb * w;
   }
 }

@@ -241,10 +241,76 @@ static bool cholesky(int n, const std::vector<double>& A, std::vector<double>& C
   return true;
 }
 
+bool gen_eig(int np, const std::vector<double>& Mv, const std::vector<double>& Bv, std::vector<double>& Sout,
+             std::vector<double>& lam, std::string& err) {
+  // Generalized eigenproblem B_v S = M_v S Lambda with S^T M_v S = I (reading Q6), by Cholesky M_v = C C^T and
+  // cyclic Jacobi on C^{-1} B_v C^{-T}.
+  std::vector<double> C;
+  if (!cholesky(np, Mv, C)) { err = "patch mass block not SPD"; return false; }
+  // K = C^{-1} B C^{-T}: solve C Y = B, then C K^T = Y^T
+  std::vector<double> Y(np * np), K(np * np);
+  for (int col = 0; col < np; ++col)
+    for (int i = 0; i < np; ++i) {
+      double s = Bv[i * np + col];
+      for (int m = 0; m < i; ++m) s -= C[i * np + m] * Y[m * np + col];
+      Y[i * np + col] = s / C[i * np + i];
+    }
+  for (int row = 0; row < np; ++row)          // K[row][:] solves C K[row]^T = Y[row]^T ... use symmetry
+    for (int i = 0; i < np; ++i) {
+      double s = Y[row * np + i];
+      for (int m = 0; m < i; ++m) s -= C[i * np + m] * K[row * np + m];
+      K[row * np + i] = s / C[i * np + i];
+    }
+  for (int i = 0; i < np; ++i)                 // symmetrize rounding
+    for (int j = 0; j < i; ++j) {
+      double a = 0.5 * (K[i * np + j] + K[j * np + i]);
+      K[i * np + j] = K[j * np + i] = a;
+    }
+  std::vector<double> w, Q;
+  jacobi_eigen(np, K, w, Q);
+  // S = C^{-T} Q  (back substitution with C^T)
+  std::vector<double> S(np * np);
+  for (int col = 0; col < np; ++col)
+    for (int i = np - 1; i >= 0; --i) {
+      double s = Q[i * np + col];
+      for (int m = i + 1; m < np; ++m) s -= C[m * np + i] * S[m * np + col];
+      S[i * np + col] = s / C[i * np + i];
+    }
+  // sort ascending, sign: largest-magnitude component positive
+  std::vector<int> idx(np);
+  for (int i = 0; i < np; ++i) idx[i] = i;
+  std::sort(idx.begin(), idx.end(), [&](int a, int b) { return w[a] < w[b]; });
+  Sout.assign(np * np, 0.0);
+  lam.assign(np, 0.0);
+  for (int c = 0; c < np; ++c) {
+    int src = idx[c];
+    if (!(w[src] > 0.0)) { err = "patch B block not positive definite (penalty too small)"; return false; }
+    int imax = 0;
+    for (int i = 1; i < np; ++i)
+      if (std::fabs(S[i * np + src]) > std::fabs(S[imax * np + src])) imax = i;
+    double sg = S[imax * np + src] < 0 ? -1.0 : 1.0;
+    for (int i = 0; i < np; ++i) Sout[i * np + c] = sg * S[i * np + src];
+    lam[c] = w[src];
+  }
+  return true;
+}
+
+static void patch_blocks(const Band& M, const Band& L, const Band& B, int k, int64_t v, std::vector<double>& Mv,
+                         std::vector<double>& Lv, std::vector<double>& Bv) {
+  const int np = 2 * k - 1;
+  const int64_t base = (v - 1) * k;
+  Mv.assign(np * np, 0.0); Lv.assign(np * np, 0.0); Bv.assign(np * np, 0.0);
+  for (int i = 0; i < np; ++i)
+    for (int j = 0; j < np; ++j) {
+      Mv[i * np + j] = M.at(base + i, base + j);
+      Bv[i * np + j] = B.at(base + i, base + j);
+      Lv[i * np + j] = L.at(base + i, base + j);
+    }
+}
+
 bool make_fdm(const RefData& rd, int64_t N, const Band& M, const Band& L, const Band& B, Fdm& out,
               std::string& err) {
-  // Generalized eigenproblem B_v S = M_v S Lambda with S^T M_v S = I (reading Q6) per axis variant,
-  // by Cholesky M_v = C C^T and cyclic Jacobi on C^{-1} B_v C^{-T}.
+  // per axis variant (translation invariance of the uniform mesh)
   const int k = rd.k, np = 2 * k - 1;
   out.np = np;
   int64_t vs[4] = {1, 2, N - 1, 1};
@@ -254,64 +320,145 @@ bool make_fdm(const RefData& rd, int64_t N, const Band& M, const Band& L, const 
   for (int var = 0; var < 4; ++var) {
     out.present[var] = pres[var];
     if (!pres[var]) continue;
-    int64_t base = (vs[var] - 1) * k;
-    std::vector<double> Mv(np * np), Bv(np * np), Lv(np * np);
-    for (int i = 0; i < np; ++i)
-      for (int j = 0; j < np; ++j) {
-        Mv[i * np + j] = M.at(base + i, base + j);
-        Bv[i * np + j] = B.at(base + i, base + j);
-        Lv[i * np + j] = L.at(base + i, base + j);
-      }
-    std::vector<double> C;
-    if (!cholesky(np, Mv, C)) { err = "patch mass block not SPD"; return false; }
-    // K = C^{-1} B C^{-T}: solve C Y = B, then C K^T = Y^T
-    std::vector<double> Y(np * np), K(np * np);
-    for (int col = 0; col < np; ++col)
-      for (int i = 0; i < np; ++i) {
-        double s = Bv[i * np + col];
-        for (int m = 0; m < i; ++m) s -= C[i * np + m] * Y[m * np + col];
-        Y[i * np + col] = s / C[i * np + i];
-      }
-    for (int row = 0; row < np; ++row)          // K[row][:] solves C K[row]^T = Y[row]^T ... use symmetry
-      for (int i = 0; i < np; ++i) {
-        double s = Y[row * np + i];
-        for (int m = 0; m < i; ++m) s -= C[i * np + m] * K[row * np + m];
-        K[row * np + i] = s / C[i * np + i];
-      }
-    for (int i = 0; i < np; ++i)                 // symmetrize rounding
-      for (int j = 0; j < i; ++j) {
-        double a = 0.5 * (K[i * np + j] + K[j * np + i]);
-        K[i * np + j] = K[j * np + i] = a;
-      }
-    std::vector<double> w, Q;
-    jacobi_eigen(np, K, w, Q);
-    // S = C^{-T} Q  (back substitution with C^T)
-    std::vector<double> S(np * np);
-    for (int col = 0; col < np; ++col)
-      for (int i = np - 1; i >= 0; --i) {
-        double s = Q[i * np + col];
-        for (int m = i + 1; m < np; ++m) s -= C[m * np + i] * S[m * np + col];
-        S[i * np + col] = s / C[i * np + i];
-      }
-    // sort ascending, sign: largest-magnitude component positive
-    std::vector<int> idx(np);
-    for (int i = 0; i < np; ++i) idx[i] = i;
-    std::sort(idx.begin(), idx.end(), [&](int a, int b) { return w[a] < w[b]; });
-    out.S[var].assign(np * np, 0.0);
-    out.lam[var].assign(np, 0.0);
-    for (int c = 0; c < np; ++c) {
-      int src = idx[c];
-      if (!(w[src] > 0.0)) { err = "patch B block not positive definite (penalty too small)"; return false; }
-      int imax = 0;
-      for (int i = 1; i < np; ++i)
-        if (std::fabs(S[i * np + src]) > std::fabs(S[imax * np + src])) imax = i;
-      double sg = S[imax * np + src] < 0 ? -1.0 : 1.0;
-      for (int i = 0; i < np; ++i) out.S[var][i * np + c] = sg * S[i * np + src];
-      out.lam[var][c] = w[src];
-    }
+    std::vector<double> Mv, Lv, Bv;
+    patch_blocks(M, L, B, k, vs[var], Mv, Lv, Bv);
+    if (!gen_eig(np, Mv, Bv, out.S[var], out.lam[var], err)) return false;
     out.Mv[var] = Mv; out.Bv[var] = Bv; out.Lv[var] = Lv;
   }
   return true;
+}
+
+bool make_fdm_vertices(int k, int64_t N, const Band& M, const Band& L, const Band& B, std::vector<double>& S,
+                       std::vector<double>& lam, std::string& err) {
+  // graded meshes: every vertex has its own patch blocks (no translation invariance), v = 1 .. N-1
+  const int np = 2 * k - 1;
+  S.assign(size_t(N - 1) * np * np, 0.0);
+  lam.assign(size_t(N - 1) * np, 0.0);
+  for (int64_t v = 1; v <= N - 1; ++v) {
+    std::vector<double> Mv, Lv, Bv, Sv, lv;
+    patch_blocks(M, L, B, k, v, Mv, Lv, Bv);
+    if (!gen_eig(np, Mv, Bv, Sv, lv, err)) return false;
+    std::copy(Sv.begin(), Sv.end(), S.begin() + (v - 1) * np * np);
+    std::copy(lv.begin(), lv.end(), lam.begin() + (v - 1) * np);
+  }
+  return true;
+}
+
+void global_bands_graded(const RefData& rd, const std::vector<double>& X, Band& M, Band& L, Band& B) {
+  // per-cell widths h_c = X[c+1] - X[c] (physical scale): M = sum h_c M^, L = sum L^ / h_c,
+  // B = sum B^ / h_c^3 + facets with the cells' own derivative scalings, interior penalty sigma / h_e with h_e the
+  // harmonic mean of the adjacent widths, boundary sigma_b / h_c (reading Q27)
+  const int k = rd.k, n1 = k + 1, hw = 2 * k, W = 2 * hw + 1;
+  const int64_t N = int64_t(X.size()) - 1, nn = k * N + 1;
+  std::vector<double> fm(nn * W, 0.0), fl(nn * W, 0.0), fbm(nn * W, 0.0);
+  auto add = [&](std::vector<double>& Xv, int64_t i, int64_t j, double val) { Xv[i * W + (j - i + hw)] += val; };
+  std::vector<double> h(N);
+  for (int64_t c = 0; c < N; ++c) h[c] = X[c + 1] - X[c];
+  for (int64_t c = 0; c < N; ++c)
+    for (int i = 0; i < n1; ++i)
+      for (int j = 0; j < n1; ++j) {
+        add(fm, c * k + i, c * k + j, h[c] * rd.Mc[i * n1 + j]);
+        add(fl, c * k + i, c * k + j, rd.Lc[i * n1 + j] / h[c]);
+        add(fbm, c * k + i, c * k + j, rd.Bc[i * n1 + j] / (h[c] * h[c] * h[c]));
+      }
+  for (int64_t f = 0; f <= N; ++f) {
+    std::vector<double> a, bb;
+    int64_t g0;
+    double pen;
+    if (f == 0) {
+      for (int m = 0; m < n1; ++m) { a.push_back(rd.la[m] / h[0]); bb.push_back(rd.lb[m] / (h[0] * h[0])); }
+      g0 = 0; pen = rd.sigma_b / h[0];
+    } else if (f == N) {
+      const double hc = h[N - 1];
+      for (int m = 0; m < n1; ++m) { a.push_back(rd.ua[m] / hc); bb.push_back(rd.ub[m] / (hc * hc)); }
+      g0 = (N - 1) * k; pen = rd.sigma_b / hc;
+    } else {
+      const double hl = h[f - 1], hr = h[f];
+      a.assign(2 * k + 1, 0.0); bb.assign(2 * k + 1, 0.0);
+      for (int m = 0; m < n1; ++m) {
+        a[m] += rd.ua[m] / hl;          bb[m] += 0.5 * rd.ub[m] / (hl * hl);
+        a[k + m] += rd.la[m] / hr;      bb[k + m] += 0.5 * rd.lb[m] / (hr * hr);
+      }
+      g0 = (f - 1) * k; pen = rd.sigma * (hl + hr) / (2.0 * hl * hr);
+    }
+    const int len = int(a.size());
+    for (int i = 0; i < len; ++i)
+      for (int j = 0; j < len; ++j) add(fbm, g0 + i, g0 + j, pen * a[i] * a[j] - a[i] * bb[j] - bb[i] * a[j]);
+  }
+  const int64_t n = nn - 2;                // eliminate nodes 0 and kN (u = 0 strongly)
+  for (Band* Xb : {&M, &L, &B}) { Xb->n = n; Xb->hw = hw; Xb->v.assign(n * W, 0.0); }
+  for (int64_t i = 0; i < n; ++i)
+    for (int qq = 0; qq < W; ++qq) {
+      int64_t j = i + qq - hw;
+      if (j < 0 || j >= n) continue;
+      M.v[i * W + qq] = fm[(i + 1) * W + qq];
+      L.v[i * W + qq] = fl[(i + 1) * W + qq];
+      B.v[i * W + qq] = fbm[(i + 1) * W + qq];
+    }
+}
+
+RectBand embedding_graded(int k, const std::vector<double>& Xf) {
+  // E_ij = phi^coarse_j(x^fine_i) on nested graded meshes (coarse boundaries = every second fine one)
+  Basis1D b = make_basis(k);
+  const int64_t Nf = int64_t(Xf.size()) - 1, Nc = Nf / 2;
+  const int64_t nf = k * Nf - 1, nc = k * Nc - 1;
+  RectBand E;
+  E.rows = nf; E.cols = nc; E.width = k + 1;
+  E.lo.assign(nf, 0);
+  E.v.assign(nf * (k + 1), 0.0);
+  std::vector<double> val(k + 1);
+  for (int64_t i = 0; i < nf; ++i) {
+    const int64_t jf = i + 1;
+    int64_t cf = jf / k, p = jf % k;
+    if (cf == Nf) { cf -= 1; p = k; }
+    const double x = Xf[cf] + b.pts[p] * (Xf[cf + 1] - Xf[cf]);
+    const int64_t cc = cf / 2;
+    const double tl = (x - Xf[2 * cc]) / (Xf[2 * cc + 2] - Xf[2 * cc]);
+    b.eval(tl, val.data(), nullptr, nullptr);
+    const int64_t lo = cc * k - 1;
+    int64_t lo_c = std::max<int64_t>(0, lo);
+    lo_c = std::min<int64_t>(lo_c, nc - (k + 1) < 0 ? 0 : nc - (k + 1));
+    E.lo[i] = lo_c;
+    for (int m = 0; m <= k; ++m) {
+      const int64_t col = lo + m;
+      if (col < 0 || col >= nc) continue;
+      double xv = val[m];
+      if (std::fabs(xv) < 1e-15) xv = 0.0;
+      const int64_t q = col - lo_c;
+      if (q >= 0 && q <= k) E.v[i * (k + 1) + q] += xv;
+    }
+  }
+  return E;
+}
+
+std::vector<double> sine_load_1d_graded(int k, const std::vector<double>& X) {
+  // f1_i = int sin(pi x) phi_i(x) dx on the graded cells, Gauss k+3 points per cell
+  Basis1D b = make_basis(k);
+  std::vector<double> qx, qw;
+  gauss_legendre(k + 3, qx, qw);
+  const int64_t N = int64_t(X.size()) - 1;
+  std::vector<double> full(k * N + 1, 0.0), v(k + 1);
+  for (int64_t c = 0; c < N; ++c) {
+    const double h = X[c + 1] - X[c];
+    for (size_t q = 0; q < qx.size(); ++q) {
+      const double x = X[c] + qx[q] * h;
+      b.eval(qx[q], v.data(), nullptr, nullptr);
+      for (int m = 0; m <= k; ++m) full[c * k + m] += h * qw[q] * std::sin(M_PI * x) * v[m];
+    }
+  }
+  return std::vector<double>(full.begin() + 1, full.end() - 1);
+}
+
+std::vector<double> boundary_normal_1d_graded(const RefData& rd, const std::vector<double>& X) {
+  const int k = rd.k;
+  const int64_t N = int64_t(X.size()) - 1;
+  const double h0 = X[1] - X[0], h1 = X[N] - X[N - 1];
+  std::vector<double> full(k * N + 1, 0.0);
+  for (int m = 0; m <= k; ++m) {
+    full[m] += (rd.sigma_b / h0) * (rd.la[m] / h0) - rd.lb[m] / (h0 * h0);
+    full[(N - 1) * k + m] += (rd.sigma_b / h1) * (rd.ua[m] / h1) - rd.ub[m] / (h1 * h1);
+  }
+  return std::vector<double>(full.begin() + 1, full.end() - 1);
 }
 
 RectBand embedding(int k, int64_t Nc) {

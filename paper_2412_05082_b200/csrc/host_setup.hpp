@@ -80,6 +80,19 @@ struct Fdm {
 bool make_fdm(const RefData& rd, int64_t N, const Band& M, const Band& L, const Band& B, Fdm& out,
               std::string& err);
 bool band_is_spd(const Band& B);
+// B_v S = M_v S Lambda, S^T M_v S = I for one patch block (ascending, sign convention of SPEC.md:320)
+bool gen_eig(int np, const std::vector<double>& Mv, const std::vector<double>& Bv, std::vector<double>& S,
+             std::vector<double>& lam, std::string& err);
+
+// ---- graded / anisotropic Cartesian meshes: X = cell boundaries of one axis (N+1 values)
+// physical-scale eliminated bands with per-cell widths and harmonic-mean facet widths
+void global_bands_graded(const RefData& rd, const std::vector<double>& X, Band& M, Band& L, Band& B);
+// per-vertex FDM factors: S[(v-1) np^2 + l np + i], lam[(v-1) np + i], v = 1 .. N-1
+bool make_fdm_vertices(int k, int64_t N, const Band& M, const Band& L, const Band& B, std::vector<double>& S,
+                       std::vector<double>& lam, std::string& err);
+RectBand embedding_graded(int k, const std::vector<double>& Xf);
+std::vector<double> sine_load_1d_graded(int k, const std::vector<double>& X);
+std::vector<double> boundary_normal_1d_graded(const RefData& rd, const std::vector<double>& X);
 
 // 1D load f1_i = int sin(pi x) phi_i(x) dx (reference scaling: includes h), Gauss k+3 pts/cell.
 std::vector<double> sine_load_1d(int k, int64_t N);
