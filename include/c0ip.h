@@ -90,6 +90,17 @@ c0ip_status c0ip_destroy(c0ip_ctx ctx);
  * c0ip_get_fdm and the exact local solver return STATE, the slab calls STATE (no fused level).  ARG for nodes that
  * do not start at 0, end at 1 or increase strictly; the arrays are copied (not retained). */
 c0ip_status c0ip_create_graded(const c0ip_config* cfg, const double* const* nodes, c0ip_ctx* out);
+
+/* The comparison workload of PAPER.md:752-816 (Fig. 5): Poisson -Delta u = f, u = 0 weakly,
+ * discontinuous Q_k with the symmetric interior penalty method (reading Q30: sigma_P = penalty_scale k(k+1) on
+ * interior facets, twice that on boundary facets, h_e = h).  DoFs: N(k+1) Gauss-Lobatto nodes per axis (cell c
+ * owns c(k+1)..c(k+1)+k), x fastest, n_dofs = (N(k+1))^d; a vertex patch holds the (2k+2)^d DoFs of its 2^d cells
+ * and its operator is exactly L_v (x) M_v + M_v (x) L_v, so the FDM local solve is exact.  Supported: c0ip_apply,
+ * c0ip_residual, c0ip_smooth (all smoothers), c0ip_restrict / c0ip_prolongate_add (DG embedding), c0ip_vcycle,
+ * c0ip_pcg, c0ip_gmres, c0ip_rhs (f = d pi^2 prod sin(pi x_a)), c0ip_get_fdm (S is (2k+2)^2), c0ip_patch_dofs
+ * ((2k+2)^d entries), c0ip_get_matrices_1d (M, L; B = L).  Generic per-axis kernels only; the slab calls and the
+ * exact local solver return STATE. */
+c0ip_status c0ip_create_sipg(const c0ip_config* cfg, c0ip_ctx* out);
 const char* c0ip_last_error(void);
 c0ip_status c0ip_set_path(c0ip_ctx ctx, c0ip_path path);
 

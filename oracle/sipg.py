@@ -190,3 +190,24 @@ def sipg_embedding_1d(k, Nc):
             tl = ((cf % 2) + t[m]) * 0.5
             E[cf * (k + 1) + m, cc * (k + 1): (cc + 1) * (k + 1)] = bas.eval(tl, 0)[:, 0]
     return E
+
+
+class SipgHierarchy:
+    """Levels 1..L of the SIPG workload (N = 2^l cells per axis) with the attributes multigrid.vcycle /
+    precondition use (Ac, ps, Pc, L, dtype): rediscretised A_l, exact patch solvers, DG embeddings P_l."""
+
+    def __init__(self, k, d, L):
+        from .mesh import level_cells
+        self.k, self.d, self.L, self.dtype = k, d, L, np.float64
+        self.Ac, self.ps, self.Pc = {}, {}, {}
+        for l in range(1, L + 1):
+            N = level_cells(l)
+            self.Ac[l] = assemble_sipg(k, d, N)
+            self.ps[l] = SipgPatchSolvers(k, d, N, self.Ac[l])
+            if l > 1:
+                E = sp.csr_matrix(sipg_embedding_1d(k, N // 2))
+                P = E
+                for _ in range(d - 1):
+                    P = sp.kron(E, P)
+                self.Pc[l] = P.tocsr()
+        self.A = self.Ac

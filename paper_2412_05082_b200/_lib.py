@@ -40,6 +40,7 @@ EXPORTS = {
     "c0ip_create": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p)]),
     "c0ip_destroy": (C.c_int, [C.c_void_p]),
     "c0ip_create_graded": (C.c_int, [C.POINTER(Config), C.c_void_p, C.POINTER(C.c_void_p)]),
+    "c0ip_create_sipg": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p)]),
     "c0ip_last_error": (C.c_char_p, []),
     "c0ip_set_path": (C.c_int, [C.c_void_p, C.c_int]),
     "c0ip_set_local_solver": (C.c_int, [C.c_void_p, C.c_int]),

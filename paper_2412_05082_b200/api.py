@@ -57,13 +57,17 @@ class MG:
 
 
 class Context:
-    def __init__(self, dim, degree, finest_level, cells_override=0, penalty_scale=1.0, device=0, nodes=None):
-        """nodes: optional per-axis cell boundaries of the finest level (graded mesh, c0ip_create_graded)."""
+    def __init__(self, dim, degree, finest_level, cells_override=0, penalty_scale=1.0, device=0, nodes=None,
+                 sipg=False):
+        """nodes: optional per-axis cell boundaries of the finest level (graded mesh, c0ip_create_graded);
+        sipg: the Poisson SIPG comparison workload (c0ip_create_sipg)."""
         self._lib = L.load()
         cfg = L.Config(int(dim), int(degree), int(finest_level), int(cells_override), float(penalty_scale),
                        int(device))
         h = C.c_void_p()
-        if nodes is None:
+        if sipg:
+            L.check(self._lib.c0ip_create_sipg(C.byref(cfg), C.byref(h)))
+        elif nodes is None:
             L.check(self._lib.c0ip_create(C.byref(cfg), C.byref(h)))
         else:
             self._nodes = [None if x is None else np.ascontiguousarray(x, dtype=np.float64) for x in nodes]
@@ -71,6 +75,7 @@ class Context:
             L.check(self._lib.c0ip_create_graded(C.byref(cfg), ptrs, C.byref(h)))
         self.h = h
         self.dim, self.degree = int(dim), int(degree)
+        self.sipg = bool(sipg)
         self.finest_level = int(finest_level)
         self.device = torch.device("cuda", int(device))
 
@@ -101,7 +106,7 @@ class Context:
         return dict(n_dofs=nd.value, n_1d=n1.value, cells=nc.value, n_patches=npch.value, n_colors=ncol.value)
 
     def patch_dofs(self, level, patch):
-        out = np.empty((2 * self.degree - 1) ** self.dim, dtype=np.int64)
+        out = np.empty((2 * self.degree + (2 if self.sipg else -1)) ** self.dim, dtype=np.int64)
         L.check(self._lib.c0ip_patch_dofs(self.h, level, patch, out.ctypes.data_as(C.c_void_p)))
         return out
 
@@ -114,7 +119,7 @@ class Context:
         return out
 
     def fdm(self, level, variant):
-        np_ = 2 * self.degree - 1
+        np_ = 2 * self.degree + (2 if self.sipg else -1)
         S = np.empty((np_, np_)); lam = np.empty(np_)
         L.check(self._lib.c0ip_get_fdm(self.h, level, variant, S.ctypes.data_as(C.c_void_p),
                                        lam.ctypes.data_as(C.c_void_p)))

@@ -126,6 +126,7 @@ struct Level {
   DevArr<int32_t> colors_d, parity_d;
   std::unique_ptr<c0ip::FusedLevel, c0ip::FusedLevelDeleter> fused;
   std::unique_ptr<ExactDev> exact;    // built on first use of the exact local solver
+  bool sipg = false;                  // Poisson SIPG level: DG numbering, A = L (x) M + M (x) L
   // graded / anisotropic Cartesian meshes: per-axis cell boundaries, bands, transfers
   bool graded = false;
   std::vector<double> nodes[3];
@@ -145,6 +146,7 @@ struct c0ip_ctx_s {
   c0ip_local_solver local = C0IP_LOCAL_FDM;
   bool graded = false;
   std::vector<double> nodes[3];                    // finest-level cell boundaries per axis (graded meshes)
+  bool sipg = false;                               // Poisson SIPG comparison workload
   std::map<std::tuple<int, int64_t, int64_t>, std::unique_ptr<WinLists>> wins;   // slab MVS patch lists
   c0ip::RefData ref;
   std::vector<Level> levels;          // index = level number (entries < lmin unused)
@@ -279,12 +281,61 @@ void ensure_tmp(Level& L, int d) {
 // globally (a slab window passes pointers shifted by -row0 * row), the per-axis temporaries are full-size
 // level arrays of which only the rows the last stage reads ([jlo - 2k, jhi + 2k)) are computed.
 template <typename T>
+c0ip::LineOp<T> band_op(const DevArr<T>& band, int hw, int64_t n) {
+  c0ip::LineOp<T> op;
+  op.v = band.p; op.lo = nullptr; op.width = 2 * hw + 1; op.hw = hw; op.n_in = n;
+  return op;
+}
+
+// Poisson SIPG: A = M_y L_x + L_y M_x (2D), M_z M_y L_x + M_z L_y M_x + L_z M_y M_x (3D)
+template <typename T>
+void sipg_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStream_t st) {
+  const int d = ctx->d, hw = 2 * ctx->k + 1;
+  const int64_t n = L.n, n2 = (d == 3) ? n : 1;
+  Tables<T>& t = tab<T>(L);
+  ensure_tmp<T>(L, d);
+  const auto Mo = band_op(t.M, hw, n), Lo = band_op(t.L, hw, n);
+  auto a0 = axis_args<T>(n, n, n2, 0, t.tmp[0].p);            // L_x x
+  add_term(a0, x, Lo, T(1));
+  launch_axis(ctx, a0, st);
+  auto a1 = axis_args<T>(n, n, n2, 0, t.tmp[1].p);            // M_x x
+  add_term(a1, x, Mo, T(1));
+  launch_axis(ctx, a1, st);
+  const T sg = b ? T(-1) : T(1);
+  if (d == 2) {
+    auto a = axis_args<T>(n, n, 1, 1, y);
+    add_term(a, (const T*)t.tmp[0].p, Mo, sg);
+    add_term(a, (const T*)t.tmp[1].p, Lo, sg);
+    if (b) { a.z = b; a.gamma = T(1); }
+    launch_axis(ctx, a, st);
+    return;
+  }
+  auto p = axis_args<T>(n, n, n, 1, t.tmp[2].p);             // P = M_y L_x x + L_y M_x x
+  add_term(p, (const T*)t.tmp[0].p, Mo, T(1));
+  add_term(p, (const T*)t.tmp[1].p, Lo, T(1));
+  launch_axis(ctx, p, st);
+  auto q = axis_args<T>(n, n, n, 1, t.tmp[3].p);             // Q = M_y M_x x
+  add_term(q, (const T*)t.tmp[1].p, Mo, T(1));
+  launch_axis(ctx, q, st);
+  auto a = axis_args<T>(n, n, n, 2, y);                      // y = M_z P + L_z Q
+  add_term(a, (const T*)t.tmp[2].p, Mo, sg);
+  add_term(a, (const T*)t.tmp[3].p, Lo, sg);
+  if (b) { a.z = b; a.gamma = T(1); }
+  launch_axis(ctx, a, st);
+}
+
+template <typename T>
 void generic_apply(c0ip_ctx ctx, Level& L, const T* x, const T* b, T* y, cudaStream_t st, int64_t jlo = 0,
                    int64_t jhi = -1) {
   const int d = ctx->d, k = ctx->k;
   const int64_t n = L.n;
   if (jhi < 0) jhi = n;
   if (jhi <= jlo) return;
+  if (L.sipg) {
+    if (jlo != 0 || jhi != n) throw std::runtime_error("SIPG levels have no windowed operator");
+    sipg_apply<T>(ctx, L, x, b, y, st);
+    return;
+  }
   Tables<T>& t = tab<T>(L);
   ensure_tmp<T>(L, d);
   // per-axis operators (identical on uniform levels; graded levels have their own per axis)
@@ -363,7 +414,8 @@ void patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, const int32_
   if (count == 0) return;
   Tables<T>& t = tab<T>(L);
   c0ip::PatchArgs<T> a{};
-  a.d = ctx->d; a.k = ctx->k; a.np = 2 * ctx->k - 1;
+  a.d = ctx->d; a.k = ctx->k; a.np = L.sipg ? 2 * ctx->k + 2 : 2 * ctx->k - 1;
+  a.pstride = L.sipg ? ctx->k + 1 : ctx->k;
   a.N = L.N; a.n = L.n;
   for (int v = 0; v < 4; ++v) { a.S[v] = t.S[v].p; a.lam[v] = t.lam[v].p; }
   for (int ax = 0; ax < 3; ++ax) {
@@ -411,7 +463,8 @@ void disjoint_patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, con
 }
 
 ExactDev& exact_tables(c0ip_ctx ctx, Level& L) {
-  if (L.graded) throw std::runtime_error("the exact local solver needs a uniform mesh (variant-tuple tables)");
+  if (L.graded || L.sipg)
+    throw std::runtime_error("the exact local solver needs a uniform C0IP level (variant-tuple tables)");
   if (!L.exact) {
     std::unique_ptr<ExactDev> e(new ExactDev());
     const int nc = 1 << (ctx->d + 1);
@@ -543,7 +596,7 @@ c0ip::LineOp<T> et_op(Level& F, int axis) {
 // fine += P coarse  (P = E (x) E (x) E, natural embedding)
 template <typename T>
 void prolongate_add_impl(c0ip_ctx ctx, Level& F, const T* coarse, T* fine, cudaStream_t st) {
-  if (ctx->path == C0IP_PATH_AUTO && ctx->d == 2 && !F.graded &&
+  if (ctx->path == C0IP_PATH_AUTO && ctx->d == 2 && !F.graded && !F.sipg &&
       c0ip::fused_transfer2d<T>(ctx->k, true, F.N / 2, coarse, fine, st, &ctx->launches))
     return;
   Tables<T>& t = tab<T>(F);
@@ -574,7 +627,7 @@ void prolongate_add_impl(c0ip_ctx ctx, Level& F, const T* coarse, T* fine, cudaS
 // coarse = P^T fine (restriction = transpose of the embedding)
 template <typename T>
 void restrict_impl(c0ip_ctx ctx, Level& F, const T* fine, T* coarse, cudaStream_t st) {
-  if (ctx->path == C0IP_PATH_AUTO && ctx->d == 2 && !F.graded &&
+  if (ctx->path == C0IP_PATH_AUTO && ctx->d == 2 && !F.graded && !F.sipg &&
       c0ip::fused_transfer2d<T>(ctx->k, false, F.N / 2, fine, coarse, st, &ctx->launches))
     return;
   Tables<T>& t = tab<T>(F);
@@ -741,12 +794,21 @@ void build_level(c0ip_ctx ctx, int l, int64_t N) {
   const int k = ctx->k, d = ctx->d;
   L.l = l;
   L.N = N;
-  L.n = k * N - 1;
+  L.sipg = ctx->sipg;
+  L.n = ctx->sipg ? N * (k + 1) : k * N - 1;           // SIPG: N (k+1) discontinuous nodes per axis
   L.h = 1.0 / double(N);
   L.ndofs = 1;
   L.npatch = 1;
   for (int a = 0; a < d; ++a) { L.ndofs *= L.n; L.npatch *= (N - 1); }
-  if (ctx->graded) {
+  if (ctx->sipg) {
+    // Poisson SIPG (reading Q30): DG mass and SIPG stiffness bands, exact FDM per variant
+    c0ip::sipg_bands(ctx->ref, N, ctx->sigma, L.M, L.L);    // sigma_P = penalty_scale k (k+1) (reading Q30)
+    L.B = L.L;
+    if (!c0ip::band_is_spd(L.L))
+      throw std::runtime_error("coercivity: 1D SIPG matrix is not positive definite (penalty too small)");
+    std::string err;
+    if (!c0ip::make_fdm_sipg(k, N, L.M, L.L, L.fdm, err)) throw std::runtime_error("coercivity: " + err);
+  } else if (ctx->graded) {
     // graded / anisotropic Cartesian mesh: per-axis bands and per-vertex FDM factors, generic
     // per-axis kernels only (the fused tile kernels assume uniform coefficients)
     L.graded = true;
@@ -811,7 +873,7 @@ void build_level(c0ip_ctx ctx, int l, int64_t N) {
   }
   L.colors_d.upload(L.colors_h);
   L.parity_d.upload(L.parity_h);
-  if (!L.graded) L.fused = c0ip::make_fused_level_impl(d, k, N, ctx->ref, L.fdm, L.h);
+  if (!L.graded && !L.sipg) L.fused = c0ip::make_fused_level_impl(d, k, N, ctx->ref, L.fdm, L.h);
 }
 
 void build_transfer(c0ip_ctx ctx, int l) {
@@ -826,7 +888,8 @@ void build_transfer(c0ip_ctx ctx, int l) {
       L.Etalo[a].upload(L.Eta[a].lo);
     }
   }
-  L.E = L.graded ? L.Ea[0] : c0ip::embedding(ctx->k, ctx->levels[l - 1].N);
+  L.E = L.sipg ? c0ip::embedding_dg(ctx->k, ctx->levels[l - 1].N)
+               : (L.graded ? L.Ea[0] : c0ip::embedding(ctx->k, ctx->levels[l - 1].N));
   L.Et = c0ip::transpose(L.E);
   L.t64.E.upload(L.E.v); L.t32.E.upload(cast_vec<float>(L.E.v));
   L.t64.Et.upload(L.Et.v); L.t32.Et.upload(cast_vec<float>(L.Et.v));
@@ -841,16 +904,18 @@ extern "C" {
 
 const char* c0ip_last_error(void) { return g_err.c_str(); }
 
-static c0ip_status create_impl(const c0ip_config* cfg, const double* const* nodes, c0ip_ctx* out);
+static c0ip_status create_impl(const c0ip_config* cfg, const double* const* nodes, bool sipg, c0ip_ctx* out);
 
-c0ip_status c0ip_create(const c0ip_config* cfg, c0ip_ctx* out) { return create_impl(cfg, nullptr, out); }
+c0ip_status c0ip_create(const c0ip_config* cfg, c0ip_ctx* out) { return create_impl(cfg, nullptr, false, out); }
+
+c0ip_status c0ip_create_sipg(const c0ip_config* cfg, c0ip_ctx* out) { return create_impl(cfg, nullptr, true, out); }
 
 c0ip_status c0ip_create_graded(const c0ip_config* cfg, const double* const* nodes, c0ip_ctx* out) {
   if (!nodes) return fail(C0IP_ERR_ARG, "null nodes");
-  return create_impl(cfg, nodes, out);
+  return create_impl(cfg, nodes, false, out);
 }
 
-static c0ip_status create_impl(const c0ip_config* cfg, const double* const* nodes, c0ip_ctx* out) {
+static c0ip_status create_impl(const c0ip_config* cfg, const double* const* nodes, bool sipg, c0ip_ctx* out) {
   if (!cfg || !out) return fail(C0IP_ERR_ARG, "null argument");
   if (cfg->dim != 2 && cfg->dim != 3) return fail(C0IP_ERR_ARG, "dim must be 2 or 3");
   if (cfg->degree < 2 || cfg->degree > 7) return fail(C0IP_ERR_ARG, "degree must be in [2,7]");
@@ -870,6 +935,7 @@ static c0ip_status create_impl(const c0ip_config* cfg, const double* const* node
   ctx->lmax = cfg->finest_level;
   ctx->lmin = cfg->cells_override > 0 ? cfg->finest_level : 1;
   ctx->levels.resize(ctx->lmax + 1);
+  ctx->sipg = sipg;
   if (nodes) {                                           // graded mesh: cell boundaries of the finest level
     const int64_t NL = cfg->cells_override > 0 ? cfg->cells_override : (int64_t(1) << cfg->finest_level);
     ctx->graded = true;
@@ -945,7 +1011,7 @@ c0ip_status c0ip_patch_dofs(c0ip_ctx ctx, int32_t level, int64_t patch, int64_t*
   if (!out) return fail(C0IP_ERR_ARG, "null output");
   Level& L = ctx->levels[level];
   if (patch < 0 || patch >= L.npatch) return fail(C0IP_ERR_ARG, "patch out of range");
-  const int d = ctx->d, k = ctx->k, np = 2 * k - 1;
+  const int d = ctx->d, k = ctx->k, np = L.sipg ? 2 * k + 2 : 2 * k - 1, ps = L.sipg ? k + 1 : k;
   int64_t v[3] = {0, 0, 0}, q = patch;
   for (int a = 0; a < d; ++a) { v[a] = 1 + q % (L.N - 1); q /= (L.N - 1); }
   const int nloc = ipow(np, d);
@@ -953,7 +1019,7 @@ c0ip_status c0ip_patch_dofs(c0ip_ctx ctx, int32_t level, int64_t patch, int64_t*
     int64_t g = 0, st = 1;
     int ll = l;
     for (int a = 0; a < d; ++a) {
-      g += ((v[a] - 1) * k + ll % np) * st;   // 1D range [(v-1)k, (v+1)k-2] (reading C2)
+      g += ((v[a] - 1) * ps + ll % np) * st;  // 1D range [(v-1)k, (v+1)k-2] (reading C2); SIPG [(v-1)(k+1), (v+1)(k+1))
       ll /= np;
       st *= L.n;
     }
@@ -1016,13 +1082,19 @@ c0ip_status c0ip_rhs(c0ip_ctx ctx, int32_t level, double* b, void* stream) {
   c0ip::LoadArgs la;
   for (int a = 0; a < 3; ++a) {
     const int aa = a < ctx->d ? a : 0;
-    tmp[a].upload(L.graded ? c0ip::sine_load_1d_graded(ctx->k, L.nodes[aa]) : c0ip::sine_load_1d(ctx->k, L.N));
-    tmpg[a].upload(L.graded ? c0ip::boundary_normal_1d_graded(ctx->ref, L.nodes[aa])
-                            : c0ip::boundary_normal_1d(ctx->ref, L.N));
+    if (L.sipg) {                                   // -Delta u* = d pi^2 prod sin, u* = 0 on the boundary
+      tmp[a].upload(c0ip::sine_load_1d_dg(ctx->k, L.N));
+      tmpg[a].upload(std::vector<double>(L.n, 0.0));
+    } else {
+      tmp[a].upload(L.graded ? c0ip::sine_load_1d_graded(ctx->k, L.nodes[aa]) : c0ip::sine_load_1d(ctx->k, L.N));
+      tmpg[a].upload(L.graded ? c0ip::boundary_normal_1d_graded(ctx->ref, L.nodes[aa])
+                              : c0ip::boundary_normal_1d(ctx->ref, L.N));
+    }
     la.f1[a] = tmp[a].p;
     la.g1[a] = tmpg[a].p;
   }
-  const double c = double(ctx->d * ctx->d) * std::pow(M_PI, 4);   // f = d^2 pi^4 prod sin (Q1, Q8)
+  const double c = L.sipg ? double(ctx->d) * M_PI * M_PI                // SIPG: f = d pi^2 prod sin
+                          : double(ctx->d * ctx->d) * std::pow(M_PI, 4);   // f = d^2 pi^4 prod sin (Q1, Q8)
   const double cb = -M_PI;                                        // g = d_n u* = -pi prod_{b!=a} sin (Q8b)
   c0ip::outer_load_kernel<<<grid_for(L.ndofs), 256, 0, st>>>(ctx->d, L.n, la, c, cb, b);
   ctx->launches++;

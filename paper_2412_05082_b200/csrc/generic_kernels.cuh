@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(256) axis_apply_kernel(AxisArgs<T> a) {
 template <typename T>
 struct PatchArgs {
   int d, k, np;
+  int pstride;            // patch origin stride per vertex: k (C0IP nodes) or k+1 (SIPG DG nodes)
   int64_t N, n;           // cells, 1D interior dofs
   const T* S[4];          // per axis variant: S[l*np + i]  (np x np)
   const T* lam[4];
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(256) patch_fdm_kernel(PatchArgs<T> a) {
     int64_t g = 0, st = 1;
     for (int ax = 0; ax < a.d; ++ax) {
       int la = l % np; l /= np;
-      g += ((vert(pid, ax) - 1) * a.k + la) * st;
+      g += ((vert(pid, ax) - 1) * a.pstride + la) * st;
       st *= a.n;
     }
     return g;

@@ -554,4 +554,104 @@ std::vector<double> boundary_normal_1d(const RefData& rd, int64_t N) {
   return std::vector<double>(full.begin() + 1, full.end() - 1);
 }
 
+// ---- Poisson SIPG comparison workload (reading Q30) ---------------------------
+void sipg_bands(const RefData& rd, int64_t N, double sigma, Band& M, Band& L) {
+  // discontinuous Q_k, cell c owns nodes c (k+1) + m; h = 1/N (physical scale): M = h M^ per cell,
+  // L = L^ / h per cell + facets (sigma_f / h) [u][v] - {u'}[v] - [u]{v'} with [u] = u^- - u^+ (normal +e of the
+  // left cell), {u'} = (u'^- + u'^+) / 2; boundary facets one-sided with penalty 2 sigma (reading Q27 convention)
+  const int k = rd.k, n1 = k + 1, hw = 2 * k + 1, W = 2 * hw + 1;
+  const int64_t n = N * n1;
+  const double h = 1.0 / double(N);
+  Basis1D b = make_basis(k);
+  std::vector<double> v0(n1), a0(n1), v1(n1), a1(n1);
+  b.eval(0.0, v0.data(), a0.data(), nullptr);
+  b.eval(1.0, v1.data(), a1.data(), nullptr);
+  for (Band* X : {&M, &L}) { X->n = n; X->hw = hw; X->v.assign(n * W, 0.0); }
+  auto add = [&](Band& X, int64_t i, int64_t j, double val) { X.v[i * W + (j - i + hw)] += val; };
+  for (int64_t c = 0; c < N; ++c)
+    for (int i = 0; i < n1; ++i)
+      for (int j = 0; j < n1; ++j) {
+        add(M, c * n1 + i, c * n1 + j, h * rd.Mc[i * n1 + j]);
+        add(L, c * n1 + i, c * n1 + j, rd.Lc[i * n1 + j] / h);
+      }
+  for (int64_t f = 0; f <= N; ++f) {
+    std::vector<double> J, D;
+    int64_t g0;
+    double pen;
+    if (f == 0) {
+      for (int m = 0; m < n1; ++m) { J.push_back(v0[m]); D.push_back(-a0[m] / h); }
+      g0 = 0; pen = 2.0 * sigma / h;
+    } else if (f == N) {
+      for (int m = 0; m < n1; ++m) { J.push_back(v1[m]); D.push_back(a1[m] / h); }
+      g0 = (N - 1) * n1; pen = 2.0 * sigma / h;
+    } else {
+      J.assign(2 * n1, 0.0); D.assign(2 * n1, 0.0);
+      for (int m = 0; m < n1; ++m) {
+        J[m] = v1[m];        D[m] = 0.5 * a1[m] / h;
+        J[n1 + m] = -v0[m];  D[n1 + m] = 0.5 * a0[m] / h;
+      }
+      g0 = (f - 1) * n1; pen = sigma / h;
+    }
+    const int len = int(J.size());
+    for (int i = 0; i < len; ++i)
+      for (int j = 0; j < len; ++j) add(L, g0 + i, g0 + j, pen * J[i] * J[j] - J[i] * D[j] - D[i] * J[j]);
+  }
+}
+
+bool make_fdm_sipg(int k, int64_t N, const Band& M, const Band& L, Fdm& out, std::string& err) {
+  // SIPG patches hold the (2k+2) DoFs of their 2 cells per axis; the patch operator is exactly L_v (x) M_v +
+  // M_v (x) L_v, so L_v S = M_v S Lambda gives the exact FDM
+  const int np = 2 * k + 2;
+  out.np = np;
+  int64_t vs[4] = {1, 2, N - 1, 1};
+  bool pres[4];
+  if (N == 2) { pres[0] = pres[1] = pres[2] = false; pres[3] = true; }
+  else { pres[0] = pres[2] = true; pres[1] = (N >= 4); pres[3] = false; }
+  for (int var = 0; var < 4; ++var) {
+    out.present[var] = pres[var];
+    if (!pres[var]) continue;
+    const int64_t base = (vs[var] - 1) * (k + 1);
+    std::vector<double> Mv(np * np), Lv(np * np);
+    for (int i = 0; i < np; ++i)
+      for (int j = 0; j < np; ++j) { Mv[i * np + j] = M.at(base + i, base + j); Lv[i * np + j] = L.at(base + i, base + j); }
+    if (!gen_eig(np, Mv, Lv, out.S[var], out.lam[var], err)) return false;
+    out.Mv[var] = Mv; out.Bv[var] = Lv; out.Lv[var] = Lv;
+  }
+  return true;
+}
+
+RectBand embedding_dg(int k, int64_t Nc) {
+  // coarse cell polynomials at the nodes of its two fine cells (block structure, width k+1)
+  Basis1D b = make_basis(k);
+  const int n1 = k + 1;
+  RectBand E;
+  E.rows = 2 * Nc * n1; E.cols = Nc * n1; E.width = n1;
+  E.lo.assign(E.rows, 0);
+  E.v.assign(E.rows * n1, 0.0);
+  std::vector<double> val(n1);
+  for (int64_t cf = 0; cf < 2 * Nc; ++cf)
+    for (int m = 0; m < n1; ++m) {
+      const int64_t i = cf * n1 + m;
+      b.eval((double(cf % 2) + b.pts[m]) * 0.5, val.data(), nullptr, nullptr);
+      E.lo[i] = (cf / 2) * n1;
+      for (int q = 0; q < n1; ++q) E.v[i * n1 + q] = std::fabs(val[q]) < 1e-15 ? 0.0 : val[q];
+    }
+  return E;
+}
+
+std::vector<double> sine_load_1d_dg(int k, int64_t N) {
+  Basis1D b = make_basis(k);
+  std::vector<double> qx, qw;
+  gauss_legendre(k + 3, qx, qw);
+  const double h = 1.0 / double(N);
+  std::vector<double> out(N * (k + 1), 0.0), v(k + 1);
+  for (int64_t c = 0; c < N; ++c)
+    for (size_t q = 0; q < qx.size(); ++q) {
+      b.eval(qx[q], v.data(), nullptr, nullptr);
+      const double fx = std::sin(M_PI * (double(c) + qx[q]) * h);
+      for (int m = 0; m <= k; ++m) out[c * (k + 1) + m] += h * qw[q] * fx * v[m];
+    }
+  return out;
+}
+
 }  // namespace c0ip

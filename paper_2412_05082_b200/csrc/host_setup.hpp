@@ -94,6 +94,13 @@ RectBand embedding_graded(int k, const std::vector<double>& Xf);
 std::vector<double> sine_load_1d_graded(int k, const std::vector<double>& X);
 std::vector<double> boundary_normal_1d_graded(const RefData& rd, const std::vector<double>& X);
 
+// ---- Poisson SIPG comparison workload (reading Q30): DG mass / SIPG stiffness bands (hw 2k+1,
+// physical scale), exact FDM per axis variant (patches of 2k+2 DoFs per axis), DG embedding, DG sine load
+void sipg_bands(const RefData& rd, int64_t N, double sigma, Band& M, Band& L);
+bool make_fdm_sipg(int k, int64_t N, const Band& M, const Band& L, Fdm& out, std::string& err);
+RectBand embedding_dg(int k, int64_t Nc);
+std::vector<double> sine_load_1d_dg(int k, int64_t N);
+
 // 1D load f1_i = int sin(pi x) phi_i(x) dx (reference scaling: includes h), Gauss k+3 pts/cell.
 std::vector<double> sine_load_1d(int k, int64_t N);
 // 1D boundary-facet factor of the Nitsche boundary data (reading Q8b): over the interior nodes,
