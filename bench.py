@@ -566,6 +566,40 @@ def sweep(d, dtype, local, degrees, clk_mhz, reps=10):
     return out
 
 
+def fig5_3d(local, reps=4):
+    """PAPER.md:809-816 (Fig. 5): operator evaluation A x and one MVS step, biharmonic C0IP vs Poisson SIPG, 3D,
+    64^3 cells, k = 2..5, FP64, as GDoF/s and the biharmonic / Poisson time ratio (the paper: 2-3x slower for the
+    biharmonic operator on an A100).  Here the C0IP path runs the fused 3D kernels, the SIPG path the generic
+    per-axis kernels (SURVEY.md f3 is a comparison workload, not tuned)."""
+    import torch
+    from paper_2412_05082_b200 import api
+    stream = torch.cuda.current_stream()
+    out = {}
+    for k in (2, 3, 4, 5):
+        row = {}
+        for name, sipg in (("biharmonic", False), ("poisson_sipg", True)):
+            ctx = api.Context(3, k, 6, device=local, sipg=sipg)
+            nd = ctx.n_dofs(6)
+            g = torch.Generator(device="cpu").manual_seed(20241205)
+            x = (torch.rand(nd, generator=g, dtype=torch.float64) * 2 - 1).cuda()
+            b = (torch.rand(nd, generator=g, dtype=torch.float64) * 2 - 1).cuda()
+            y = torch.empty_like(x)
+            t_mv = _time_ms(lambda: ctx.apply(6, x, y), reps, stream)
+            om = 0.7 if not sipg else 1.0
+            t_mvs = _time_ms(lambda: ctx.smooth(6, "mvs", 1, om, b, x), max(2, reps // 2), stream)
+            row[name] = {"dofs": nd, "ax_gdofs": round(nd / (t_mv * 1e-3) / 1e9, 3), "ax_ms": round(t_mv, 4),
+                         "mvs_gdofs": round(nd / (t_mvs * 1e-3) / 1e9, 3), "mvs_ms": round(t_mvs, 4)}
+            ctx.close()
+            del x, b, y
+            torch.cuda.empty_cache()
+        row["biharmonic_over_poisson_time_per_dof"] = {
+            "ax": round(row["poisson_sipg"]["ax_gdofs"] / row["biharmonic"]["ax_gdofs"], 3),
+            "mvs": round(row["poisson_sipg"]["mvs_gdofs"] / row["biharmonic"]["mvs_gdofs"], 3)}
+        out[f"k{k}"] = row
+    out["config"] = "3D unit cube, 64^3 cells (level 6), FP64; MVS omega 0.7 (C0IP) / 1 (SIPG, exact FDM)"
+    return out
+
+
 def mixed_3d(local):
     """The paper's mixed-precision experiment (Fig. 4): 3D, GMRES preconditioned by the
     V-cycle with one MVS step (omega 0.7, same-order cycle), FP64 cycle vs FP32 cycle (outer FGMRES(30) in FP64),
@@ -823,6 +857,25 @@ def main():
         res["mixed_speedup"] = round(res["fp64"]["seconds"] / res["mixed"]["seconds"], 3)
         line["pcg"] = res
         cp.close()
+        if d == 2:
+            # the largest 2D level at which the FP32 cycle keeps the FP64 iteration count within 1 (DESIGN.md §8:
+            # u32 kappa(A) grows like h^-4; 2D k=4: L = 9)
+            Lh = Lp - 1
+            ch = api.Context(d, k, Lh, device=local)
+            bh = ch.rhs(Lh)
+            rh = {}
+            for name, cdt in (("fp64", torch.float64), ("mixed", torch.float32)):
+                mg = api.MG("avs", 2, 0.25, cycle_dtype=cdt)
+                ch.pcg(mg, bh, max_iter=3)
+                torch.cuda.synchronize()
+                xs, rep, hist = ch.pcg(mg, bh)
+                rh[name] = {"seconds": round(rep["seconds"], 4), "iterations": rep["iterations"],
+                            "nu": round(rep["nu"], 2), "converged": rep["converged"]}
+            rh["dofs"] = ch.n_dofs(Lh)
+            rh["level"] = Lh
+            rh["mixed_speedup"] = round(rh["fp64"]["seconds"] / rh["mixed"]["seconds"], 3)
+            line["pcg_mixed_holds"] = rh
+            ch.close()
         if (d == 2 and k == 4) or d == 3:
             # cfg3 (BASELINE.json configs[2]): coloured multiplicative smoother, k = 4, N = 2048 (67.1M DoFs),
             # one MVS step (omega = 0.8, reading Q28) with the symmetric colour order (Q11), FP32 vs
@@ -866,6 +919,8 @@ def main():
 
     if not args.no_pcg and world == 1 and d == 2:
         line["mixed_3d"] = mixed_3d(local)
+    if not args.no_sweep and world == 1 and d == 2:
+        line["fig5_3d"] = fig5_3d(local)
     if not args.no_sweep and world == 1:
         line["sweep_2d"] = sweep(2, args.dtype, local, range(2, 8), clk_mhz)
         line["sweep_3d_cfg4"] = sweep(3, args.dtype, local, range(2, 6), clk_mhz, reps=4)
