@@ -230,6 +230,13 @@ c0ip_status c0ip_slab_avs_step(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, doubl
                                int64_t lrows, int64_t out_lo, int64_t out_hi, const void* b_ext,
                                void* x_ext, void* r_ext, void* stream);
 
+/* The update half of c0ip_slab_avs_step: x_ext += omega sum_v R_v^T A~_v^{-1} R_v r on the owned rows [out_lo,
+ * out_hi), reading r_ext on the owned rows +- (2k-2) (which the caller computed with c0ip_slab_apply).  Splitting
+ * the step as residual(interior rows) | halo exchange | residual(boundary rows) | c0ip_slab_fdm overlaps the
+ * exchange with the interior residual and gives the same owned rows as c0ip_slab_avs_step, bitwise. */
+c0ip_status c0ip_slab_fdm(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, double omega, int64_t row0, int64_t lrows,
+                          int64_t out_lo, int64_t out_hi, const void* r_ext, void* x_ext, void* stream);
+
 /* y = A x (b_ext == NULL) or r = b - A x on the owned rows of a slab window (ghosts of width 2k). */
 c0ip_status c0ip_slab_apply(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, int64_t row0, int64_t lrows,
                             int64_t out_lo, int64_t out_hi, const void* b_ext, const void* x_ext,

@@ -65,6 +65,8 @@ EXPORTS = {
     "c0ip_gmres": (C.c_int, [C.c_void_p, C.POINTER(MgConfig), C.c_void_p, C.c_void_p, C.c_double, C.c_int32,
                              C.c_int32, C.POINTER(Report), C.c_void_p, C.c_void_p]),
     "c0ip_launch_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "c0ip_slab_fdm": (C.c_int, [C.c_void_p, C.c_int32, C.c_int, C.c_double, C.c_int64, C.c_int64, C.c_int64,
+                                C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "c0ip_slab_mvs_color": (C.c_int, [C.c_void_p, C.c_int32, C.c_int, C.c_double, C.c_int32, C.c_int64, C.c_int64,
                                       C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "c0ip_slab_restrict": (C.c_int, [C.c_void_p, C.c_int32, C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,

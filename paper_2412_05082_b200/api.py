@@ -249,6 +249,12 @@ class Context:
                                           _ptr(y_ext), _stream()))
         return y_ext
 
+    def slab_fdm(self, level, omega, row0, lrows, out_lo, out_hi, r_ext, x_ext):
+        _check(x_ext, self._slab_n(level, lrows), r_ext)
+        L.check(self._lib.c0ip_slab_fdm(self.h, level, _dtype(x_ext), float(omega), int(row0), int(lrows), int(out_lo),
+                                        int(out_hi), _ptr(r_ext), _ptr(x_ext), _stream()))
+        return x_ext
+
     def slab_mvs_color(self, level, omega, color, row0, lrows, out_lo, out_hi, b_ext, x_ext, r_ext):
         _check(x_ext, self._slab_n(level, lrows), b_ext, r_ext)
         L.check(self._lib.c0ip_slab_mvs_color(self.h, level, _dtype(x_ext), float(omega), int(color), int(row0),

@@ -1435,6 +1435,32 @@ c0ip_status c0ip_slab_avs_step(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, doubl
   ABI_CATCH
 }
 
+c0ip_status c0ip_slab_fdm(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, double omega, int64_t row0, int64_t lrows,
+                          int64_t out_lo, int64_t out_hi, const void* r_ext, void* x_ext, void* stream) {
+  c0ip_status s = check_level(ctx, level);
+  if (s) return s;
+  if (!r_ext || !x_ext) return fail(C0IP_ERR_ARG, "null vector");
+  Level& L = ctx->levels[level];
+  if ((s = check_window(ctx, L, row0, lrows, out_lo, out_hi, 2 * ctx->k - 2))) return s;
+  ABI_TRY
+  cudaStream_t st = (cudaStream_t)stream;
+  c0ip::SlabWindow wo{row0, lrows, out_lo, out_hi};
+  const bool three = c0ip::fused_dim(*L.fused) == 3;
+  if (dt == C0IP_F64) {
+    if (three) c0ip::fused3_fdm_window<double>(*L.fused, omega, (const double*)r_ext, (double*)x_ext, false, st,
+                                               &ctx->launches, &wo);
+    else c0ip::fused_fdm<double>(*L.fused, omega, (const double*)r_ext, (double*)x_ext, st, &ctx->launches, &wo);
+  } else if (dt == C0IP_F32) {
+    if (three) c0ip::fused3_fdm_window<float>(*L.fused, (float)omega, (const float*)r_ext, (float*)x_ext, false, st,
+                                              &ctx->launches, &wo);
+    else c0ip::fused_fdm<float>(*L.fused, (float)omega, (const float*)r_ext, (float*)x_ext, st, &ctx->launches, &wo);
+  } else {
+    return fail(C0IP_ERR_ARG, "bad dtype");
+  }
+  return C0IP_OK;
+  ABI_CATCH
+}
+
 c0ip_status c0ip_slab_apply(c0ip_ctx ctx, int32_t level, c0ip_dtype dt, int64_t row0, int64_t lrows, int64_t out_lo,
                             int64_t out_hi, const void* b_ext, const void* x_ext, void* y_ext, void* stream) {
   c0ip_status s = check_level(ctx, level);

@@ -113,6 +113,58 @@ def exchange(x_ext, slab, row_len, group=None):
     return nbytes
 
 
+def start_exchange(x_ext, slab, row_len, group=None):
+    """Post the ghost-row exchange without waiting (NCCL: the receive completes on NCCL's stream); returns a
+    finisher that makes the current stream wait for it.  gloo with CUDA tensors (one-GPU tests) is host-staged
+    and completes here."""
+    import torch.distributed as dist
+    if slab.nranks == 1:
+        return lambda: None
+    if _host_staged(x_ext) or dist.get_backend() == "gloo":
+        exchange(x_ext, slab, row_len, group)
+        return lambda: None
+    g = slab.ghost
+    rows = x_ext.view(-1, row_len)
+    lo_ghost, hi_ghost = slab.own_lo - slab.win_lo, slab.win_hi - slab.own_hi
+    ops = []
+    if slab.rank > 0 and lo_ghost > 0:
+        ops.append(dist.P2POp(dist.isend, rows[lo_ghost:lo_ghost + g], slab.rank - 1, group))
+        ops.append(dist.P2POp(dist.irecv, rows[0:lo_ghost], slab.rank - 1, group))
+    if slab.rank < slab.nranks - 1 and hi_ghost > 0:
+        top = slab.own_hi - slab.win_lo
+        ops.append(dist.P2POp(dist.isend, rows[top - g:top], slab.rank + 1, group))
+        ops.append(dist.P2POp(dist.irecv, rows[top:top + hi_ghost], slab.rank + 1, group))
+    works = dist.batch_isend_irecv(ops) if ops else []
+
+    def finish():
+        for w in works:
+            w.wait()
+    return finish
+
+
+def avs_step_overlapped(ctx, level, omega, slab, row_len, b_ext, x_ext, r_ext, group=None):
+    """One additive smoothing step on a slab with the halo exchange overlapped (SURVEY.md §8e "Overlap"): the
+    residual of the interior owned rows (whose stencil needs no ghost row) runs while the ghost rows travel;
+    then the residual of the two boundary strips and the FDM update (c0ip_slab_fdm).  Same result as
+    c0ip_slab_avs_step, bitwise."""
+    k = ctx.degree
+    s = slab
+    KN = k * s.N
+    finish = start_exchange(x_ext, s, row_len, group)
+    in_lo, in_hi = s.own_lo + 2 * k, s.own_hi - 2 * k
+    r_lo, r_hi = max(1, s.own_lo - (2 * k - 2)), min(KN, s.own_hi + 2 * k - 2)
+    if in_hi > in_lo:
+        ctx.slab_apply(level, s.row0, s.lrows, in_lo, in_hi, x_ext, r_ext, b_ext=b_ext)
+    finish()
+    if in_hi > in_lo:
+        ctx.slab_apply(level, s.row0, s.lrows, r_lo, in_lo, x_ext, r_ext, b_ext=b_ext)
+        ctx.slab_apply(level, s.row0, s.lrows, in_hi, r_hi, x_ext, r_ext, b_ext=b_ext)
+    else:
+        ctx.slab_apply(level, s.row0, s.lrows, r_lo, r_hi, x_ext, r_ext, b_ext=b_ext)
+    ctx.slab_fdm(level, omega, s.row0, s.lrows, s.own_lo, s.own_hi, r_ext, x_ext)
+    return x_ext
+
+
 def allreduce_sum(vals, device, group=None):
     import torch
     import torch.distributed as dist
@@ -187,8 +239,8 @@ class DistMG:
                     self._xchg(lev, x)
                     self.ctx.slab_mvs_color(lev.level, self.omega, c, s.row0, s.lrows, s.own_lo, s.own_hi, b, x, lev.r)
             else:
-                self._xchg(lev, x)
-                self.ctx.slab_avs_step(lev.level, self.omega, s.row0, s.lrows, s.own_lo, s.own_hi, b, x, lev.r)
+                self.exchanges += 1
+                avs_step_overlapped(self.ctx, lev.level, self.omega, s, lev.row, b, x, lev.r, self.group)
 
     def residual(self, lev, x, b, r):
         """owned rows of r = b - A x (ghosts of x exchanged first)"""

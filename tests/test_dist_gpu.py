@@ -130,3 +130,34 @@ def test_distributed_pcg_matches_oracle(d, k, L, kind, steps, omega):
     xg = xg.ravel()
     assert np.linalg.norm(xg - xo) <= 1e-6 * np.linalg.norm(xo)
     assert np.linalg.norm(bo - h.A[L] @ xg) <= 1.05e-8 * np.linalg.norm(bo)
+
+
+def _avs_overlap(rank, world, d, k, N, omega):
+    import torch
+    from paper_2412_05082_b200 import api
+    from paper_2412_05082_b200.dist import partition, exchange, avs_step_overlapped
+    from c0ip_inputs import random_xb
+    ctx = api.Context(d, k, 3, cells_override=N)
+    n = k * N - 1
+    row = n ** (d - 1)
+    x, b = random_xb(k, d, N)
+    s = partition(N, k, world, 4 * k - 2)[rank]
+    rows = slice(s.row0, s.row0 + s.lrows)
+    xw = torch.tensor(x.reshape(-1, row)[rows].ravel(), device="cuda:0")
+    bw = torch.tensor(b.reshape(-1, row)[rows].ravel(), device="cuda:0")
+    rw = torch.empty_like(xw)
+    x2 = xw.clone()
+    avs_step_overlapped(ctx, 3, omega, s, row, bw, xw, rw)
+    exchange(x2, s, row)
+    ctx.slab_avs_step(3, omega, s.row0, s.lrows, s.own_lo, s.own_hi, bw, x2, torch.empty_like(x2))
+    own, ref = xw.view(-1, row)[s.own_local].cpu().numpy(), x2.view(-1, row)[s.own_local].cpu().numpy()
+    ctx.close()
+    return bool(np.array_equal(own, ref))
+
+
+@pytest.mark.parametrize("d,k,N,omega", [(2, 4, 32, 0.25), (2, 3, 40, 0.25), (3, 2, 16, 0.1), (3, 3, 16, 0.1)])
+def test_overlapped_avs_step_equals_slab_step(d, k, N, omega):
+    """Residual of the interior rows during the halo exchange, boundary strips after it, then c0ip_slab_fdm:
+    bitwise the same owned rows as c0ip_slab_avs_step."""
+    out = _run("_avs_overlap", 2, d, k, N, omega)
+    assert all(out.values()), out
