@@ -343,3 +343,79 @@ class DistPCG:
             ctx.axpby(1.0, o(z), rz_new / rz, o(p))
             rz = rz_new
         return x, n, hist
+
+
+class DistGMRES:
+    """Flexible right-preconditioned GMRES(m) in FP64 on slabs (the paper's outer solver for the
+    multiplicative smoother; c0ip_gmres on one GPU): Arnoldi with classical Gram-Schmidt and one
+    re-orthogonalisation (CGS2: the j+1 projections of a step are one all-reduce), Givens rotations on the host,
+    the preconditioner is DistMG.cycle (same-order MVS cycle when symmetric=False).  Vectors are windows of the
+    finest level; every vector update runs in the library (c0ip_vec_axpby / c0ip_vec_dots on the owned rows)."""
+
+    def __init__(self, mgd, restart=30):
+        self.m = mgd
+        self.lev = mgd.levels[mgd.ctx.finest_level]
+        self.restart = restart
+
+    def _dots(self, pairs):
+        o = self.lev.owned
+        vals = []
+        for i in range(0, len(pairs), 2):
+            chunk = pairs[i:i + 2]
+            if len(chunk) == 2:
+                vals += list(self.m.ctx.dots(o(chunk[0][0]), o(chunk[0][1]), o(chunk[1][0]), o(chunk[1][1])))
+            else:
+                vals += list(self.m.ctx.dots(o(chunk[0][0]), o(chunk[0][1])))
+        return allreduce_sum(vals, self.m.device, self.m.group)
+
+    def solve(self, b_ext, rtol=1e-8, max_iter=200):
+        import math
+        import torch
+        ctx, lev, o = self.m.ctx, self.lev, self.lev.owned
+        x = torch.zeros_like(b_ext)
+        w = torch.zeros_like(b_ext)
+        V = [torch.zeros_like(b_ext) for _ in range(self.restart + 1)]
+        Z = [torch.zeros_like(b_ext) for _ in range(self.restart)]
+        self.m.residual(lev, x, b_ext, V[0])
+        beta = math.sqrt(self._dots([(V[0], V[0])])[0])
+        r0, rn, hist, it = beta, beta, [beta], 0
+        while it < max_iter and rn > rtol * r0 and beta > 0:
+            mm = min(self.restart, max_iter - it)
+            ctx.axpby(0.0, o(V[0]), 1.0 / beta, o(V[0]))
+            H = [[0.0] * mm for _ in range(mm + 1)]
+            cs, sn, g = [0.0] * mm, [0.0] * mm, [0.0] * (mm + 1)
+            g[0] = beta
+            jd = 0
+            for j in range(mm):
+                self.m.cycle(lev.level, Z[j], V[j])
+                self.m.apply(lev, Z[j], w)
+                for _ in range(2):                                   # CGS2
+                    hs = self._dots([(w, V[i]) for i in range(j + 1)])
+                    for i in range(j + 1):
+                        H[i][j] += hs[i]
+                        ctx.axpby(-hs[i], o(V[i]), 1.0, o(w))
+                H[j + 1][j] = math.sqrt(self._dots([(w, w)])[0])
+                ctx.axpby(1.0 / H[j + 1][j] if H[j + 1][j] > 0 else 0.0, o(w), 0.0, o(V[j + 1]))
+                for i in range(j):
+                    t = cs[i] * H[i][j] + sn[i] * H[i + 1][j]
+                    H[i + 1][j] = -sn[i] * H[i][j] + cs[i] * H[i + 1][j]
+                    H[i][j] = t
+                den = math.hypot(H[j][j], H[j + 1][j])
+                cs[j], sn[j] = H[j][j] / den, H[j + 1][j] / den
+                H[j][j], H[j + 1][j] = den, 0.0
+                g[j + 1] = -sn[j] * g[j]
+                g[j] = cs[j] * g[j]
+                it += 1
+                jd = j + 1
+                rn = abs(g[j + 1])
+                hist.append(rn)
+                if rn <= rtol * r0:
+                    break
+            y = [0.0] * jd
+            for i in range(jd - 1, -1, -1):
+                y[i] = (g[i] - sum(H[i][l] * y[l] for l in range(i + 1, jd))) / H[i][i]
+            for i in range(jd):
+                ctx.axpby(y[i], o(Z[i]), 1.0, o(x))
+            self.m.residual(lev, x, b_ext, V[0])
+            beta = math.sqrt(self._dots([(V[0], V[0])])[0])
+        return x, it, hist

@@ -91,17 +91,17 @@ def test_slab_mvs_step_bitwise_equals_single_domain(d, k, N, omega):
         assert np.array_equal(own, full[lo - 1: hi - 1]), r
 
 
-def _pcg(rank, world, d, k, L, kind, steps, omega):
+def _pcg(rank, world, d, k, L, kind, steps, omega, solver="cg"):
     import torch
     from paper_2412_05082_b200 import api
-    from paper_2412_05082_b200.dist import DistMG, DistPCG
+    from paper_2412_05082_b200.dist import DistMG, DistPCG, DistGMRES
     ctx = api.Context(d, k, L)
     b = ctx.rhs(L)
-    mg = DistMG(ctx, kind, steps, omega, symmetric=True)
+    mg = DistMG(ctx, kind, steps, omega, symmetric=(solver == "cg"))
     lev = mg.levels[L]
     s = lev.slab
     bw = b.view(-1, lev.row)[s.row0: s.row0 + s.lrows].reshape(-1).clone()
-    x, n, hist = DistPCG(mg).solve(bw)
+    x, n, hist = (DistPCG(mg) if solver == "cg" else DistGMRES(mg)).solve(bw)
     own = lev.owned(x).cpu().numpy()
     res = (s.own_lo, s.own_hi, own, n, hist, sorted(mg.levels), mg.exchanges)
     ctx.close()
@@ -161,3 +161,25 @@ def test_overlapped_avs_step_equals_slab_step(d, k, N, omega):
     bitwise the same owned rows as c0ip_slab_avs_step."""
     out = _run("_avs_overlap", 2, d, k, N, omega)
     assert all(out.values()), out
+
+
+@pytest.mark.parametrize("d,k,L,omega", [(2, 4, 5, 0.8), (3, 2, 4, 0.7)])
+def test_distributed_gmres_mvs_matches_oracle(d, k, L, omega):
+    """The paper's MVS protocol on 2 slabs: FGMRES around the same-order (nonsymmetric) MVS V-cycle with colours in
+    lockstep; iteration count within 1 of the oracle's FGMRES, gathered solution at the tolerance."""
+    from oracle.multigrid import Hierarchy, gmres, precondition
+    from oracle.operator import paper_rhs
+    from oracle.discretization import default_sigma
+    out = _run("_pcg", 2, d, k, L, "mvs", 1, omega, "gmres")
+    s = default_sigma(k)
+    h = Hierarchy(k, d, L, s)
+    bo = paper_rhs(k, d, 2 ** L, s)
+    xo, no, ho = gmres(h.A[L], bo, lambda r: precondition(h, r, "mvs", 1, omega, symmetric=False))
+    row = (k * 2 ** L - 1) ** (d - 1)
+    xg = np.zeros_like(xo).reshape(-1, row)
+    for r, (lo, hi, own, n, hist, levels, nx) in out.items():
+        assert abs(n - no) <= 1, (r, n, no)
+        xg[lo - 1: hi - 1] = own.reshape(-1, row)
+    xg = xg.ravel()
+    floor = 32 * 2.2e-16 * np.linalg.norm(abs(h.A[L]) @ np.abs(xg))        # SURVEY.md F9 rounding floor
+    assert np.linalg.norm(bo - h.A[L] @ xg) <= 1.05e-8 * np.linalg.norm(bo) + floor
