@@ -198,7 +198,8 @@ c0ip_status c0ip_pcg(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, do
 
 /* MG-preconditioned flexible GMRES(m) in FP64 (GMRES is the paper's
  * outer solver for the multiplicative smoother, whose same-order V-cycle (mg->symmetric = 0) is not
- * symmetric).  Right preconditioning z_j = MG(v_j) (c0ip_vcycle), modified Gram-Schmidt Arnoldi,
+ * symmetric).  Right preconditioning z_j = MG(v_j) (c0ip_vcycle), Arnoldi by classical Gram-Schmidt with one
+ * re-orthogonalisation (CGS2: batched projections, three host round trips per step),
  * Givens rotations, restart after `restart` steps (the device holds restart+1 Krylov vectors and
  * restart preconditioned vectors of the finest level: (2 restart + 2) * 8 n bytes, owned by the ctx).
  * x (device FP64, in: x0, out: solution), b device FP64.  Stops when the least-squares residual

@@ -152,7 +152,7 @@ struct c0ip_ctx_s {
   std::vector<Level> levels;          // index = level number (entries < lmin unused)
   int64_t launches = 0;
   DevArr<double> pcg_r, pcg_z, pcg_p, pcg_Ap, dot_part, dot_out;
-  DevArr<double> gm_V, gm_Z, gm_w;                 // GMRES: Krylov basis, preconditioned basis, work
+  DevArr<double> gm_V, gm_Z, gm_w, gm_h;           // GMRES: Krylov basis, preconditioned basis, work, projections
   const double* vc_r = nullptr;                    // buffers the captured V-cycle graph reads / writes
   double* vc_z = nullptr;
   double* dot_host = nullptr;
@@ -185,7 +185,7 @@ struct c0ip_ctx_s {
       L.exact.reset();
     }
     pcg_r.free(); pcg_z.free(); pcg_p.free(); pcg_Ap.free(); dot_part.free(); dot_out.free();
-    gm_V.free(); gm_Z.free(); gm_w.free();
+    gm_V.free(); gm_Z.free(); gm_w.free(); gm_h.free();
     if (dot_host) cudaFreeHost(dot_host);
   }
 };
@@ -1259,6 +1259,33 @@ c0ip_status c0ip_pcg(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, do
   ABI_CATCH
 }
 
+// w -= V (V^T w) over the nv basis vectors V_0..V_{nv-1} (classical Gram-Schmidt pass): batched dots (8 vectors
+// per pass over w), one host round trip, batched update (64 vectors per pass); hs = V^T w
+static void project(c0ip_ctx ctx, int64_t n, int nv, double* w, const double* V, std::vector<double>& hs,
+                    cudaStream_t st) {
+  const int G = 296;
+  ctx->dot_part.alloc(8 * G);
+  ctx->gm_h.alloc(nv);
+  for (int c0 = 0; c0 < nv; c0 += 8) {
+    const int cnt = std::min(8, nv - c0);
+    c0ip::mdot_partial_kernel<8><<<G, 256, 0, st>>>(n, cnt, w, V + size_t(c0) * n, ctx->dot_part.p);
+    c0ip::mdot_final_kernel<<<cnt, 256, 0, st>>>(G, ctx->dot_part.p, ctx->gm_h.p + c0);
+    ctx->launches += 2;
+  }
+  CK(cudaGetLastError());
+  hs.assign(nv, 0.0);
+  CK(cudaMemcpyAsync(hs.data(), ctx->gm_h.p, nv * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int c0 = 0; c0 < nv; c0 += 64) {
+    const int cnt = std::min(64, nv - c0);
+    c0ip::Coefs64 cf{};
+    for (int c = 0; c < cnt; ++c) cf.c[c] = hs[c0 + c];
+    c0ip::maxpy_kernel<<<grid_for(n), 256, 0, st>>>(n, cnt, cf, V + size_t(c0) * n, w);
+    ctx->launches++;
+  }
+  CK(cudaGetLastError());
+}
+
 c0ip_status c0ip_gmres(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, double* x, double rtol,
                        int32_t max_iter, int32_t restart, c0ip_report* rep, double* res_history, void* stream) {
   c0ip_status s = check_mg(ctx, mg);
@@ -1272,7 +1299,8 @@ c0ip_status c0ip_gmres(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, 
   const int64_t n = L.ndofs;
   const int m = restart;          // workspace sized by restart (reused across calls: no allocation
                                   // inside a timed solve after the first call with this restart)
-  // Flexible right-preconditioned GMRES(m) (Saad Alg. 9.6), modified Gram-Schmidt, Givens rotations
+  // Flexible right-preconditioned GMRES(m) (Saad Alg. 9.6), classical Gram-Schmidt with one re-orthogonalisation
+  // (CGS2: two batched projections and one norm per Arnoldi step = 3 host round trips), Givens rotations
   // (GMRES outer solver for the multiplicative smoother)
   ctx->gm_V.alloc(n * (m + 1));
   ctx->gm_Z.alloc(n * m);
@@ -1316,10 +1344,11 @@ c0ip_status c0ip_gmres(c0ip_ctx ctx, const c0ip_mg_config* mg, const double* b, 
         CK(cudaMemcpyAsync(zj, ctx->pcg_z.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
       }
       apply_op<double>(ctx, L, zj, nullptr, w, st);              // w = A z_j
-      for (int i = 0; i <= j; ++i) {                             // modified Gram-Schmidt
-        dots(ctx, n, 1, w, V + size_t(i) * n, nullptr, nullptr, nullptr, nullptr, dd, st);
-        h(i, j) = dd[0];
-        axpby<double>(ctx, n, -dd[0], V + size_t(i) * n, 1.0, w, st);
+      for (int i = 0; i <= j; ++i) h(i, j) = 0.0;
+      for (int pass = 0; pass < 2; ++pass) {                     // CGS2: two batched projection passes
+        std::vector<double> hs;
+        project(ctx, n, j + 1, w, V, hs, st);
+        for (int i = 0; i <= j; ++i) h(i, j) += hs[i];
       }
       dots(ctx, n, 1, w, w, nullptr, nullptr, nullptr, nullptr, dd, st);
       h(j + 1, j) = std::sqrt(dd[0]);

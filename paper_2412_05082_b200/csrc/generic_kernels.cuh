@@ -270,6 +270,60 @@ __global__ void __launch_bounds__(256) dot_final_kernel(int nparts, const double
     for (int j = 0; j < 3; ++j) out[j] = sh[j][0];
 }
 
+// Batched projections of the GMRES Arnoldi step (classical Gram-Schmidt, CGS2): partial sums of <w, V_c> for
+// c < nv (<= CH) in one pass over w (block partials in fixed order: deterministic), then one final reduction
+// per vector, and w -= sum_c coef_c V_c in one pass.
+template <int CH>
+__global__ void __launch_bounds__(256) mdot_partial_kernel(int64_t n, int nv, const double* __restrict__ w,
+                                                           const double* __restrict__ V, double* partial) {
+  __shared__ double sh[CH][256];
+  double acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc[c] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double wi = w[i];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (c < nv) acc[c] += wi * V[c * n + i];
+  }
+#pragma unroll
+  for (int c = 0; c < CH; ++c) sh[c][threadIdx.x] = acc[c];
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+#pragma unroll
+      for (int c = 0; c < CH; ++c) sh[c][threadIdx.x] += sh[c][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x < nv && threadIdx.x < CH) partial[threadIdx.x * gridDim.x + blockIdx.x] = sh[threadIdx.x][0];
+}
+
+__global__ void __launch_bounds__(256) mdot_final_kernel(int G, const double* partial, double* out) {
+  __shared__ double sh[256];
+  double s = 0;
+  for (int i = threadIdx.x; i < G; i += blockDim.x) s += partial[blockIdx.x * G + i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = sh[0];
+}
+
+struct Coefs64 {
+  double c[64];
+};
+
+__global__ void maxpy_kernel(int64_t n, int nv, const __grid_constant__ Coefs64 cf, const double* __restrict__ V,
+                             double* __restrict__ w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = w[i];
+    for (int c = 0; c < nv; ++c) s -= cf.c[c] * V[c * n + i];
+    w[i] = s;
+  }
+}
+
 // b[g] = c * prod_a f1[i_a] + cb * sum_a g1[i_a] prod_{b != a} f1[i_b]
 // (separable paper load plus the separable Nitsche boundary data, reading Q8b)
 // (per-axis 1D factors f1[a], g1[a]: graded meshes have different ones per axis)
