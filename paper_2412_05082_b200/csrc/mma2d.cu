@@ -527,6 +527,7 @@ __global__ void __launch_bounds__(256, 4) patch_fdm2d_mma_kernel(const __grid_co
       const int vary = vy == 1 ? 0 : (vy == Nm1 ? 2 : 1);
       int64_t po = int64_t((vy - 1) * K + g) * n + (vx0 - 1) * K + 2 * q;
       double b0 = r0 ? __ldg(r + po) : 0.0, b1 = r1 ? __ldg(r + po + 1) : 0.0;
+      double h0 = 0.0, h1 = 0.0;                         // this lane's columns held for the next patch
 #pragma unroll 1
       for (int vx = vx0; vx < vx1; ++vx) {
         double nb0 = 0.0, nb1 = 0.0;
@@ -542,8 +543,27 @@ __global__ void __launch_bounds__(256, 4) patch_fdm2d_mma_kernel(const __grid_co
           patch_solve(ffs[varx][lane], ffs[vary][lane], sfs[varx * 3 + vary][lane], b0, b1, u0, u1);
         }
         double* xp = P.x + po;
-        if (r0) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp), "d"(u0) : "memory");
-        if (r1) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp + 1), "d"(u1) : "memory");
+        if constexpr (K % 2 == 0) {
+          // consecutive patches of the run overlap in K - 1 columns: the previous patch's columns >= K (lanes
+          // q >= S) are this patch's columns < K (lanes q - S) -- merge them in registers and issue one atomic
+          // per node row and column of the overlap instead of two ((2k-1)/k instead of ((2k-1)/k)^2 atomics
+          // per DoF along x)
+          constexpr int S = K / 2;
+          const double s0 = __shfl_down_sync(0xffffffffu, h0, S), s1 = __shfl_down_sync(0xffffffffu, h1, S);
+          if (q + S <= 3) { u0 += s0; u1 += s1; }
+          if (q < S || vx + 1 == vx1) {                  // columns no later patch of the run touches
+            if (r0) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp), "d"(u0) : "memory");
+            if (r1) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp + 1), "d"(u1) : "memory");
+            h0 = 0.0;
+            h1 = 0.0;
+          } else {
+            h0 = u0;
+            h1 = u1;
+          }
+        } else {
+          if (r0) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp), "d"(u0) : "memory");
+          if (r1) asm volatile("red.global.add.f64 [%0], %1;" ::"l"(xp + 1), "d"(u1) : "memory");
+        }
         po += K;
         b0 = nb0;
         b1 = nb1;
