@@ -36,10 +36,10 @@ namespace c0ip {
 
 // register-blocking factor of a stage with `lines` lines per unit column and `mult` unit columns:
 // minimise rounds(rb) * rb over 256 threads (the per-thread work of a stage), prefer larger rb on ties
-__host__ __device__ constexpr int pick_rb(int lines, int mult, int maxrb) {
+__host__ __device__ constexpr int pick_rb(int lines, int mult, int maxrb, int nt = 256) {
   int best = 1, bestc = 1 << 30;
   for (int rb = 1; rb <= maxrb; ++rb) {
-    const int cost = cdiv(cdiv(lines, rb) * mult, 256) * rb;
+    const int cost = cdiv(cdiv(lines, rb) * mult, nt) * rb;
     if (cost <= bestc) { bestc = cost; best = rb; }
   }
   return best;
@@ -108,42 +108,44 @@ __device__ __forceinline__ void y_all_interior(const Coef2<T, K>& c, const T (&w
 }
 
 // ----------------------------------------------------------------------------- apply2d
-template <typename T, int K>
+template <typename T, int K, int NT_>
 struct ApplyLayout {
+  static constexpr int NT = NT_;                   // threads per CTA
   static constexpr int C = Tile<K>::C, O = Tile<K>::O, RB = Blk<T, K>::RB;
   static constexpr int BW = (C + 3) * K + 1;       // box: nodes [(c0-2)K, (c0+C+1)K]
   static constexpr int PX = odd(BW), PO = odd(O);
-  static constexpr int XB = BW * PX, BB = O * PO;  // box, b tile
   static constexpr int XN = O * PX;                // the O new box rows of a tile below the previous one
   static constexpr int STAGE = BW * PO;            // one of the three x-stage outputs
-  static constexpr int TOTAL = XB + 2 * XN + 2 * BB + 3 * STAGE;
+  // the full box of a chunk's first tile lives in the two new-row buffers (2 O >= BW rows); b is read
+  // from global memory in the epilogue (streamed once, issued before the y-stage contractions)
+  static_assert(2 * O >= BW, "first box must fit the two new-row buffers");
+  static constexpr int TOTAL = 2 * XN + 3 * STAGE;
   // register blocking: the column-walk stages have few units (O rows x C cells); for FP64 k = 4 blocking
-  // RB lines per thread (one LDCU per RB DFMA, half the threads idle) measured faster than the balanced
-  // choice of pick_rb, for the other degrees and FP32 slower (0.205 -> 0.196 ms at k = 4)
+  // RB lines per thread (one LDCU per RB DFMA) and 128-thread CTAs (every thread busy, 3 CTAs per SM)
   static constexpr bool FORCE = (K == 4 && sizeof(T) == 8);
-  static constexpr int RBX = pick_rb(BW, C, RB), RBY = FORCE ? RB : pick_rb(O, C, RB);
-  static constexpr int RBXN = FORCE ? RB : pick_rb(O, C, RB);   // x-stage on the O new rows only
+  static constexpr int RBX = pick_rb(BW, C, RB, NT), RBY = FORCE ? RB : pick_rb(O, C, RB, NT);
+  static constexpr int RBXN = FORCE ? RB : pick_rb(O, C, RB, NT);   // x-stage on the O new rows only
   static_assert(BW - O <= O, "carried rows must not overlap the rows they are copied from");
   static constexpr int GX = cdiv(BW, RBX);         // row groups of the x-stage
   static constexpr int GY = cdiv(O, RBY);          // column groups of the y-stage
+  static constexpr int MINB = NT == 128 ? 3 : 2;   // CTAs per SM
 };
 
-template <typename T, int K>
-__global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__ ApplyP<T, K> P) {
+template <typename T, int K, int NT_>
+__global__ void __launch_bounds__(NT_, ApplyLayout<T, K, NT_>::MINB) apply2d_kernel(const __grid_constant__ ApplyP<T, K> P) {
   // Work item = (tile column tx, chunk of CH tile rows): the CTA walks down the chunk.  Consecutive
   // tiles of a column share BW - O box rows; their x-stage outputs are carried over (shifted up in
   // shared memory), so only the O new box rows are loaded and contracted per tile after the first.
-  using LY = ApplyLayout<T, K>;
+  using LY = ApplyLayout<T, K, NT_>;
   constexpr int C = LY::C, O = LY::O, BW = LY::BW, PX = LY::PX, PO = LY::PO;
   const int CH = P.chunk;                        // tiles per column chunk (host: ~8 items per CTA)
   constexpr int GY = LY::GY;
-  constexpr int NT = 256;
+  constexpr int NT = LY::NT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
-  T* const xfull = sm;                           // [XB]   full box of a chunk's first tile
-  T* const xnew0 = sm + LY::XB;                  // [2][XN] new rows of the following tiles
-  T* const bbuf0 = xnew0 + 2 * LY::XN;           // [2][BB]
-  T* sB = bbuf0 + 2 * LY::BB;
+  T* const xnew0 = sm;                           // [2][XN] new rows of a tile; [BW][PX] full box of a chunk's first tile
+  T* const xfull = xnew0;
+  T* sB = xnew0 + 2 * LY::XN;
   T* sL = sB + LY::STAGE;
   T* sM = sL + LY::STAGE;
   const int64_t N = P.N, n = P.n, KN = K * N;
@@ -155,9 +157,6 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
   const int tid = threadIdx.x;
   int round = 0;
 
-  auto load_b = [&](int64_t cx0, int64_t cy0, int buf) {
-    if (P.b) load_box_async<T, O, O, PO>(bbuf0 + buf * LY::BB, P.b, n, KN, cy0 * K, cx0 * K, P.row0, P.lrows);
-  };
   auto load_new = [&](int64_t cx0, int64_t cy0, int buf) {   // box rows [BW - O, BW) of tile row cy0
     load_box_async<T, O, BW, PX>(xnew0 + buf * LY::XN, P.x, n, KN, (cy0 - 2) * K + (BW - O), (cx0 - 2) * K,
                                  P.row0, P.lrows);
@@ -167,17 +166,15 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
     const int tx = item % ntx, ch = item / ntx;
     const int tA = ty0 + ch * CH, tB = min(tA + CH, ty1);
     const int64_t cx0 = int64_t(tx) * C;
-    // first tile of the chunk: full box (synchronous), b tile
+    // first tile of the chunk: full box (synchronous) in both new-row buffers
     load_box_async<T, BW, BW, PX>(xfull, P.x, n, KN, (int64_t(tA) * C - 2) * K, (cx0 - 2) * K, P.row0, P.lrows);
-    load_b(cx0, int64_t(tA) * C, 0);
     cp_async_commit();
     int buf = 0;
     for (int ty = tA; ty < tB; ++ty) {
       const bool first = (ty == tA);
-      if (ty + 1 < tB) {                       // prefetch the next tile's new rows and b tile
-        load_new(cx0, int64_t(ty + 1) * C, buf ^ 1);
-        load_b(cx0, int64_t(ty + 1) * C, buf ^ 1);
-      }
+      // prefetch the next tile's new rows into the other buffer (after the first tile: once its x-stage
+      // has consumed the box, which occupies both buffers)
+      if (!first && ty + 1 < tB) load_new(cx0, int64_t(ty + 1) * C, buf ^ 1);
       cp_async_commit();
       cp_async_wait1();
       if (!first) {                            // carry the x-stage rows shared with the previous tile
@@ -191,7 +188,6 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
       }
       __syncthreads();
       const T* xsrc = first ? xfull : xnew0 + buf * LY::XN;
-      const T* bt = bbuf0 + buf * LY::BB;
       const int64_t cy0 = int64_t(ty) * C;
     const bool tin = (cx0 >= 2 && cx0 + C - 1 <= N - 2 && cy0 >= 2 && cy0 + C - 1 <= N - 2);
     auto tile_body = [&](auto INC) {
@@ -267,6 +263,10 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
     if (first) xstage(std::integral_constant<int, BW>{}, std::integral_constant<int, LY::RBX>{});
     else xstage(std::integral_constant<int, O>{}, std::integral_constant<int, LY::RBXN>{});
     __syncthreads();
+    if (first && ty + 1 < tB) {                // the box is consumed: prefetch the next tile's new rows
+      load_new(cx0, int64_t(ty + 1) * C, 1);
+      cp_async_commit();
+    }
 
     // y-stage: y = h^-2 (B^_y (M^_x x) + M^_y (B^_x x) + 2 L^_y (L^_x x)).  lanes <-> column
     // groups; three passes (one window at a time) accumulate K outputs for RB columns.
@@ -288,6 +288,20 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
       int col[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) col[r] = min(g + r * GY, O - 1);
+      // b of the unit's outputs (read once from global memory; issued before the contractions)
+      T bv[K][RB];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int cc = g + r * GY;
+        const int64_t jx = cx0 * K + cc;
+        const bool okc = cc < O && (IN || (jx >= 1 && jx <= KN - 1));
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const int64_t j = cy * K + p;
+          const bool ok = P.b && okc && j >= P.out_lo && j < P.out_hi;
+          bv[p][r] = ok ? P.b[(j - 1 - P.row0) * n + (jx - 1)] : T(0);
+        }
+      }
       if (inner) {
         T accL[K][RB];
 #pragma unroll
@@ -378,7 +392,7 @@ __global__ void __launch_bounds__(256, 2) apply2d_kernel(const __grid_constant__
           const int64_t j = cy * K + p;
           if (j < P.out_lo || j >= P.out_hi) continue;   // (slab window; always true for the full domain)
           const T v = P.scale * acc[p][r];
-          P.y[(j - 1 - P.row0) * n + (jx - 1)] = P.b ? bt[(ci * K + p) * PO + cc] - v : v;
+          P.y[(j - 1 - P.row0) * n + (jx - 1)] = P.b ? bv[p][r] - v : v;
         }
       }
     }
@@ -1058,23 +1072,23 @@ std::unique_ptr<FusedLevel, FusedLevelDeleter> make_fused_level_impl(int d, int 
 
 
 template <typename KernelT>
-static int persistent_grid(KernelT kern, size_t smem, int ntiles) {
+static int persistent_grid(KernelT kern, size_t smem, int ntiles, int nt = 256) {
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, nt, smem);
   return std::max(1, std::min(ntiles, sms * std::max(per, 1)));
 }
 
-template <typename T, int K>
-static void launch_apply(const FusedLevel& F, const T* x, const T* b, T* y, const SlabWindow& w, cudaStream_t st) {
-  using LY = ApplyLayout<T, K>;
+template <typename T, int K, int NT>
+static void launch_apply_nt(const FusedLevel& F, const T* x, const T* b, T* y, const SlabWindow& w, cudaStream_t st) {
+  using LY = ApplyLayout<T, K, NT>;
   const size_t smem = sizeof(T) * size_t(LY::TOTAL);
   static int grid_cache = -1;
   if (grid_cache < 0) {
-    cudaFuncSetAttribute(apply2d_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(apply2d_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    grid_cache = persistent_grid(apply2d_kernel<T, K>, smem, 1 << 30);
+    cudaFuncSetAttribute(apply2d_kernel<T, K, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(apply2d_kernel<T, K, NT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    grid_cache = persistent_grid(apply2d_kernel<T, K, NT>, smem, 1 << 30, NT);
   }
   ApplyP<T, K> p;
   std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
@@ -1089,7 +1103,20 @@ static void launch_apply(const FusedLevel& F, const T* x, const T* b, T* y, cons
   p.chunk = int(std::max<int64_t>(1, (nty + want - 1) / want));
   const int64_t nch = (nty + p.chunk - 1) / p.chunk;
   const int grid = (int)std::min<int64_t>(grid_cache, ntx * nch);
-  apply2d_kernel<T, K><<<grid, 256, smem, st>>>(p);
+  apply2d_kernel<T, K, NT><<<grid, NT, smem, st>>>(p);
+}
+
+// CTA size: 128 threads where the register-blocked column-walk stages have ~128 units (FP64 k = 4),
+// 256 otherwise; C0IP_APPLY_NT overrides (measurement knob)
+template <typename T, int K>
+static void launch_apply(const FusedLevel& F, const T* x, const T* b, T* y, const SlabWindow& w, cudaStream_t st) {
+  static const int nt = [] {
+    const char* e = std::getenv("C0IP_APPLY_NT");
+    if (e) return std::atoi(e) == 128 ? 128 : 256;
+    return (K == 4 && sizeof(T) == 8) ? 128 : 256;
+  }();
+  if (nt == 128) launch_apply_nt<T, K, 128>(F, x, b, y, w, st);
+  else launch_apply_nt<T, K, 256>(F, x, b, y, w, st);
 }
 
 template <typename T, int K>
