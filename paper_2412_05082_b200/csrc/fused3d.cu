@@ -5,10 +5,11 @@
 //                  and a chunk of CZ cell layers along z and streams through z: per cell layer it
 //                  builds, for K new node planes, the in-plane results
 //                    P = B^_y M^_x + M^_y B^_x + 2 L^_y L^_x,  Q = L^_y M^_x + M^_y L^_x,  R = M^_y M^_x
-//                  (x- and y-stages in shared memory) and each thread, owning one in-plane node, keeps
-//                  sliding register windows of P, Q, R along z and emits
+//                  (x- and y-stages in shared memory); each thread, owning one in-plane node, adds
+//                  every arriving plane of P, Q, R into the 4K + 1 pending outputs of its z column
 //                    y = M^_z P + 2 L^_z Q + B^_z R
-//                  for the finished cell layer (output-centric banded rows, uniform coefficients).
+//                  (scatter form of the banded z rows, uniform coefficients) and emits the finished
+//                  cell layer.
 //   patch_fdm3d  : x += omega h A~_v^{-1} R_v r for a list of patches: per patch the
 //                  six 1D contractions (S^T along x, y, z; divide by lambda_x + lambda_y + lambda_z; S
 //                  along z, y, x) with one thread per patch line and register-blocked lines.  Launched
@@ -74,33 +75,31 @@ __device__ __forceinline__ T row_band(F coef, const T* w, int base) {
 }
 
 // K node planes z0 .. z0+K-1 of the in-plane box into smem (cp.async, zero fill outside the domain)
-// (node plane jz lives at local plane jz - 1 - row0, valid for local planes [0, lrows))
+// (node plane jz lives at local plane jz - 1 - row0, valid for local planes [0, lrows)).  Thread t copies
+// elements t, t + 256, ... of the K x BW x BW box: the element -> (plane, row, column) split is by
+// compile-time constants and the 64-bit base address is formed once per call, so a box that lies inside
+// the domain (every CTA but the boundary ones) costs a few integer instructions per element.
 template <typename T, int K, int BW, int PX>
 __device__ __forceinline__ void load_planes_async(T* dst, const T* src, int64_t n, int64_t KN, int64_t z0,
                                                   int64_t Y0, int64_t X0, int64_t row0, int64_t lrows) {
+  constexpr int TOT = K * BW * BW;
   const int64_t zlo = (row0 + 1 > 1) ? row0 + 1 : int64_t(1), zhi = (row0 + lrows < KN - 1) ? row0 + lrows : KN - 1;
   const bool inner = (X0 >= 1 && X0 + BW - 1 <= KN - 1 && Y0 >= 1 && Y0 + BW - 1 <= KN - 1 && z0 >= zlo &&
                       z0 + K - 1 <= zhi);
-  // one warp per (plane, box row), lanes along the row: the 64-bit row address once per row
   const T* base = src + ((z0 - 1 - row0) * n + (Y0 - 1)) * n + (X0 - 1);
-  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const bool xin = (X0 >= 1 && X0 + BW - 1 <= KN - 1);
-  for (int pr = threadIdx.x >> 5; pr < K * BW; pr += nw) {
-    const int pz = pr / BW, r = pr - pz * BW;
-    const T* rowp = base + ((int64_t)pz * n + r) * n;
-    T* d = dst + (pz * BW + r) * PX;
-    const int64_t jz = z0 + pz, jy = Y0 + r;
-    const bool rok = inner || (jy >= 1 && jy <= KN - 1 && jz >= zlo && jz <= zhi);
-    if (inner || (rok && xin)) {
-#pragma unroll
-      for (int cc = lane; cc < BW; cc += 32) cp_async_elem(d + cc, rowp + cc, true);
-    } else {
-#pragma unroll
-      for (int cc = lane; cc < BW; cc += 32) {
-        const int64_t jx = X0 + cc;
-        const bool ok = rok && jx >= 1 && jx <= KN - 1;
-        cp_async_elem(d + cc, ok ? rowp + cc : src, ok);
-      }
+  const int nn = int(n);
+  if (inner) {
+#pragma unroll 4
+    for (int e = threadIdx.x; e < TOT; e += 256) {
+      const int pz = e / (BW * BW), rc = e - pz * (BW * BW), r = rc / BW, cc = rc - r * BW;
+      cp_async_elem(dst + (pz * BW + r) * PX + cc, base + ((int64_t)pz * nn + r) * nn + cc, true);
+    }
+  } else {
+    for (int e = threadIdx.x; e < TOT; e += 256) {
+      const int pz = e / (BW * BW), rc = e - pz * (BW * BW), r = rc / BW, cc = rc - r * BW;
+      const int64_t jz = z0 + pz, jy = Y0 + r, jx = X0 + cc;
+      const bool ok = jz >= zlo && jz <= zhi && jy >= 1 && jy <= KN - 1 && jx >= 1 && jx <= KN - 1;
+      cp_async_elem(dst + (pz * BW + r) * PX + cc, ok ? base + ((int64_t)pz * nn + r) * nn + cc : src, ok);
     }
   }
 }
@@ -122,11 +121,21 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
   const int tid = threadIdx.x;
   const int oy = tid / O, ox = tid - (tid / O) * O;       // z-stage ownership (tid < O*O)
   const bool zown = tid < O * O;
-  T wR[4 * K + 1], wP[3 * K + 1], wQ[3 * K + 1];
+  // z-stage, two forms (measured per degree):
+  //  * scatter (k = 3): acc[i] <-> output node plane (cn - 2) K + i, i in [0, 4K], where cn is the cell
+  //    layer whose K node planes ((cn-1)K, cnK] arrive at this step; every arriving plane adds its P, Q, R
+  //    values to the outputs within the band (M^_z, 2 L^_z, B^_z), and layer cn - 2 is complete.  4K + 1
+  //    live registers instead of 10K + 3 (frees the registers for XR = 2 in the x-stage at 2 CTAs/SM);
+  //  * windows (k = 2, 4, 5): sliding register windows of P, Q, R along z, output-centric banded rows.
+  constexpr bool SCAT = (K == 3);
+  T acc[SCAT ? 4 * K + 1 : 1];
 #pragma unroll
-  for (int i = 0; i <= 4 * K; ++i) wR[i] = 0;
+  for (int i = 0; i < (SCAT ? 4 * K + 1 : 1); ++i) acc[i] = 0;
+  T wR[SCAT ? 1 : 4 * K + 1], wP[SCAT ? 1 : 3 * K + 1], wQ[SCAT ? 1 : 3 * K + 1];
 #pragma unroll
-  for (int i = 0; i <= 3 * K; ++i) wP[i] = wQ[i] = 0;
+  for (int i = 0; i < (SCAT ? 1 : 4 * K + 1); ++i) wR[i] = 0;
+#pragma unroll
+  for (int i = 0; i < (SCAT ? 1 : 3 * K + 1); ++i) wP[i] = wQ[i] = 0;
   int round = 0;
   const int nsteps = int(std::min<int64_t>(CZ, P.cz_hi - cz0)) + 4;
 
@@ -144,10 +153,10 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
     const T* xb = xb0 + (s & 1) * LY::XB;
 
     // x-stage: unit = (plane, box row group, cell) -> B^ L^ M^ along x for the K nodes of the cell;
-    // rows hr, hr + HB, ... (XR rows) share every coefficient load (register blocking; XR = 1 for FP64
-    // k = 3, where the second row spills at the 2-CTA register budget -- measured)
+    // rows hr, hr + HB, ... (XR rows) share every coefficient load (register blocking; fits the 2-CTA
+    // register budget at every degree since the z-stage holds 4K + 1 accumulators instead of windows)
     {
-      constexpr int XR = (K == 3 && sizeof(T) == 8) ? 1 : 2;
+      constexpr int XR = (K == 3 && sizeof(T) == 8 && !SCAT) ? 1 : 2;
       constexpr int HB = cdiv(BW, XR);
 #pragma unroll 1
       for (int it = 0; it < cdiv(K * HB * C, NT); ++it, ++round) {
@@ -248,47 +257,112 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
     }
     __syncthreads();
 
-    // z-stage: shift the windows by K planes, append the new ones, emit the finished cell layer
-    if (zown) {
+    if constexpr (SCAT) {
+      // z-stage (scatter form, see acc above): the K planes appended now are (cn-1)K + 1 + pz, cn = cz0 - 2 + s
+      const int64_t cn = cz0 - 2 + s, cz = cn - 2;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      if (zown) {
+        // every output node of the pending range is an interior-class row unless the range meets the
+        // boundary rows j <= K or j >= KN - K (uniform over the CTA)
+        const bool zin = (cn - 2) * K > K && (cn + 2) * K < KN - K;
 #pragma unroll
-      for (int i = 0; i <= 3 * K; ++i) wR[i] = wR[i + K];
+        for (int pz = 0; pz < K; ++pz) {
+          const T vP = pqr[((pz * 3 + 0) * O + oy) * O + ox];
+          const T vQ = T(2) * pqr[((pz * 3 + 1) * O + oy) * O + ox];
+          const T vR = pqr[((pz * 3 + 2) * O + oy) * O + ox];
 #pragma unroll
-      for (int i = 0; i <= 2 * K; ++i) { wP[i] = wP[i + K]; wQ[i] = wQ[i + K]; }
-#pragma unroll
-      for (int pz = 0; pz < K; ++pz) {
-        wP[2 * K + 1 + pz] = pqr[((pz * 3 + 0) * O + oy) * O + ox];
-        wQ[2 * K + 1 + pz] = pqr[((pz * 3 + 1) * O + oy) * O + ox];
-        wR[3 * K + 1 + pz] = pqr[((pz * 3 + 2) * O + oy) * O + ox];
+          for (int i = 0; i <= 4 * K; ++i) {
+            const int d = K + 1 + pz - i;              // input plane - output plane
+            const int po = i % K;                      // class of the output node
+            const int qb = d + 2 * K, qm = d + K;      // B index (offsets -2K..2K), M/L index (-K..K)
+            const bool nzb = qb >= 0 && qb <= 4 * K && (po == 0 || (qb >= K - po && qb <= 4 * K - po));
+            const bool nzm = qm >= 0 && qm <= 2 * K && (po == 0 || (qm >= K - po && qm <= 2 * K - po));
+            if (!nzb && !nzm) continue;
+            if (zin) {
+              if (nzb) acc[i] = fma(c.BI[po][nzb ? qb : 0], vR, acc[i]);
+              if (nzm) {
+                acc[i] = fma(c.MI[po][nzm ? qm : 0], vP, acc[i]);
+                acc[i] = fma(c.LI[po][nzm ? qm : 0], vQ, acc[i]);
+              }
+            } else {
+              const int sp = special_row<K>((cn - 2) * K + i, N);
+              if (sp < 0) {
+                if (nzb) acc[i] = fma(c.BI[po][nzb ? qb : 0], vR, acc[i]);
+                if (nzm) {
+                  acc[i] = fma(c.MI[po][nzm ? qm : 0], vP, acc[i]);
+                  acc[i] = fma(c.LI[po][nzm ? qm : 0], vQ, acc[i]);
+                }
+              } else if (qb >= 0 && qb <= 4 * K) {       // special rows: offsets -2K..2K, zero padded
+                acc[i] = fma(c.BS[sp][qb], vR, acc[i]);
+                acc[i] = fma(c.MS[sp][qb], vP, acc[i]);
+                acc[i] = fma(c.LS[sp][qb], vQ, acc[i]);
+              }
+            }
+          }
+        }
       }
-    }
-    // after this step the newest plane is (cz0 - 2 + s) K: layer cz = cz0 + s - 4 is complete
-    const int64_t cz = cz0 + s - 4;
-    const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
-    if (s >= 4 && zown) {
-      const int64_t jx = cx0 * K + ox, jy = cy0 * K + oy;
-      if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1) {
-        const bool inner = (cz >= 2 && cz <= N - 2);
+      // layer cz = cn - 2 is complete (emitted for cz >= cz0, i.e. s >= 4)
+      if (s >= 4 && zown) {
+        const int64_t jx = cx0 * K + ox, jy = cy0 * K + oy;
+        if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1) {
 #pragma unroll
-        for (int p = 0; p < K; ++p) {
-          const int64_t jz = cz * K + p;
-          if (jz < P.out_lo || jz >= P.out_hi) continue;
-          const int sp = inner ? -1 : special_row<K>(jz, N);
-          T v = 0;
-          // windows: wR[i] <-> plane (cz-2)K + i ; wP/wQ[i] <-> plane (cz-1)K + i
-          with_p<K>(p, [&](auto PC) {
-            constexpr int PP = decltype(PC)::value;
-            if (sp < 0)
-              v = row_band<T, K, PP, 4 * K + 1>([&](int q) { return c.BI[PP][q]; }, wR, 0) +
-                  row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MI[PP][q]; }, wP, 0) +
-                  T(2) * row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LI[PP][q]; }, wQ, 0);
-            else
-              v = row_band<T, K, PP, 4 * K + 1>([&](int q) { return c.BS[sp][q]; }, wR, 0) +
-                  row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MS[sp][q + K]; }, wP, 0) +
-                  T(2) * row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LS[sp][q + K]; }, wQ, 0);
-          });
-          const int64_t g = ((jz - 1 - P.row0) * n + (jy - 1)) * n + (jx - 1);
-          v *= P.scale;
-          P.y[g] = P.b ? P.b[g] - v : v;
+          for (int p = 0; p < K; ++p) {
+            const int64_t jz = cz * K + p;
+            if (jz < P.out_lo || jz >= P.out_hi) continue;
+            const int64_t g = ((jz - 1 - P.row0) * n + (jy - 1)) * n + (jx - 1);
+            const T v = acc[p] * P.scale;
+            P.y[g] = P.b ? P.b[g] - v : v;
+          }
+        }
+      }
+      // shift the pending outputs by one cell layer
+#pragma unroll
+      for (int i = 0; i <= 3 * K; ++i) acc[i] = acc[i + K];
+#pragma unroll
+      for (int i = 3 * K + 1; i <= 4 * K; ++i) acc[i] = 0;
+    } else {
+      // z-stage: shift the windows by K planes, append the new ones, emit the finished cell layer
+      if (zown) {
+#pragma unroll
+        for (int i = 0; i <= 3 * K; ++i) wR[i] = wR[i + K];
+#pragma unroll
+        for (int i = 0; i <= 2 * K; ++i) { wP[i] = wP[i + K]; wQ[i] = wQ[i + K]; }
+#pragma unroll
+        for (int pz = 0; pz < K; ++pz) {
+          wP[2 * K + 1 + pz] = pqr[((pz * 3 + 0) * O + oy) * O + ox];
+          wQ[2 * K + 1 + pz] = pqr[((pz * 3 + 1) * O + oy) * O + ox];
+          wR[3 * K + 1 + pz] = pqr[((pz * 3 + 2) * O + oy) * O + ox];
+        }
+      }
+      // after this step the newest plane is (cz0 - 2 + s) K: layer cz = cz0 + s - 4 is complete
+      const int64_t cz = cz0 + s - 4;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      if (s >= 4 && zown) {
+        const int64_t jx = cx0 * K + ox, jy = cy0 * K + oy;
+        if (jx >= 1 && jx <= KN - 1 && jy >= 1 && jy <= KN - 1) {
+          const bool inner = (cz >= 2 && cz <= N - 2);
+#pragma unroll
+          for (int p = 0; p < K; ++p) {
+            const int64_t jz = cz * K + p;
+            if (jz < P.out_lo || jz >= P.out_hi) continue;
+            const int sp = inner ? -1 : special_row<K>(jz, N);
+            T v = 0;
+            // windows: wR[i] <-> plane (cz-2)K + i ; wP/wQ[i] <-> plane (cz-1)K + i
+            with_p<K>(p, [&](auto PC) {
+              constexpr int PP = decltype(PC)::value;
+              if (sp < 0)
+                v = row_band<T, K, PP, 4 * K + 1>([&](int q) { return c.BI[PP][q]; }, wR, 0) +
+                    row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MI[PP][q]; }, wP, 0) +
+                    T(2) * row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LI[PP][q]; }, wQ, 0);
+              else
+                v = row_band<T, K, PP, 4 * K + 1>([&](int q) { return c.BS[sp][q]; }, wR, 0) +
+                    row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.MS[sp][q + K]; }, wP, 0) +
+                    T(2) * row_band<T, K, PP, 2 * K + 1>([&](int q) { return c.LS[sp][q + K]; }, wQ, 0);
+            });
+            const int64_t g = ((jz - 1 - P.row0) * n + (jy - 1)) * n + (jx - 1);
+            v *= P.scale;
+            P.y[g] = P.b ? P.b[g] - v : v;
+          }
         }
       }
     }
