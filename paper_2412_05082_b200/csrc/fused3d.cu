@@ -713,6 +713,177 @@ __global__ void __launch_bounds__(256, (K == 3 && sizeof(T) == 8) ? 3 : 4) patch
   }
 }
 
+// ----------------------------------------------------------------------------- patch_fdm3d_run (k <= 3)
+// Atomic AVS patch solves x += omega h A~_v^{-1} R_v r for runs of PW consecutive
+// patches along x (same vy, vz): NP = 2K - 1 lanes per patch, PW = 32 / NP patches per warp; lane (p, m)
+// holds the node plane z = m of patch p (NP x NP values in registers).  S_x^T and S_y^T (and S_y, S_x on the
+// way back) contract the lane's plane in registers; the z stage (S_z^T, 1 / (lam_x + lam_y + lam_z), S_z)
+// runs after one transpose through a per-warp shared buffer, lane m then holding the z lines
+// t = m, m + NP, ... of its patch.  Consecutive patches of a run overlap in K - 1 node columns: lane
+// (p + 1, m) hands those columns to lane (p, m) (warp shuffles), which adds them before its red.global.add,
+// so the run updates every node column once per plane ((2k-1)/k instead of ((2k-1)/k)^3 atomics per DoF
+// along x).  Interior runs take coefficients as warp-uniform kernel-parameter operands; runs touching the
+// boundary read per-lane variants from a shared copy.
+template <typename T, int K>
+struct Fdm3RunLayout {
+  static constexpr int NP = 2 * K - 1, NP2 = NP * NP, PW = 32 / NP, LANES = PW * NP;
+  static constexpr int PL = NP2 | 1;               // odd plane pitch (conflict-free plane stores)
+  static constexpr int WB = LANES * PL;            // per-warp transpose buffer
+  static constexpr int TAB = NP2 * NP;             // interior 1 / (lx + ly + lz), index (m NP + j) NP + i
+  static constexpr int TOTAL = 8 * WB + TAB + 3 * NP2 + 3 * NP;
+};
+
+// out = S^T w (TR) or S w (!TR) of one line, coefficients from coef(idx) with idx = l NP + i
+template <int NP, bool TR, typename T, typename F>
+__device__ __forceinline__ void line_mul(F coef, const T (&w)[NP], T (&o)[NP]) {
+#pragma unroll
+  for (int i = 0; i < NP; ++i) o[i] = 0;
+#pragma unroll
+  for (int l = 0; l < NP; ++l)
+#pragma unroll
+    for (int i = 0; i < NP; ++i) o[i] = fma(coef(TR ? l * NP + i : i * NP + l), w[l], o[i]);
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(256, 2) patch_fdm3d_run_kernel(const __grid_constant__ Fdm3P<T, K> P) {
+  using LY = Fdm3RunLayout<T, K>;
+  constexpr int NP = LY::NP, NP2 = LY::NP2, PW = LY::PW, PL = LY::PL;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* const sm = reinterpret_cast<T*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T* const buf = sm + warp * LY::WB;
+  T* const tab = sm + 8 * LY::WB;
+  T* const sS = tab + LY::TAB;                     // [3][NP2] S of the variants
+  T* const sL = sS + 3 * NP2;                      // [3][NP]  lambda of the variants
+  for (int e = tid; e < LY::TAB; e += 256) {
+    const int i = e % NP, j = (e / NP) % NP, m = e / NP2;
+    tab[e] = T(1) / (P.c.lam[1][i] + P.c.lam[1][j] + P.c.lam[1][m]);
+  }
+  for (int e = tid; e < 3 * NP2; e += 256) sS[e] = P.c.S[e / NP2][e % NP2];
+  for (int e = tid; e < 3 * NP; e += 256) sL[e] = P.c.lam[e / NP][e % NP];
+  __syncthreads();
+  const int64_t N = P.N, n = P.n;
+  const int nvx = P.vcnt[0], nvy = P.vcnt[1], nvz = P.vcnt[2];
+  const int runs_x = (nvx + PW - 1) / PW;
+  const int64_t nruns = int64_t(runs_x) * nvy * nvz;
+  const int p = lane / NP, m = lane - (lane / NP) * NP;
+  const int64_t wstride = int64_t(gridDim.x) * 8;
+  int round = 0;
+#pragma unroll 1
+  for (int64_t run = int64_t(blockIdx.x) * 8 + warp; run < nruns; run += wstride, ++round) {
+    const int64_t rz = run / (int64_t(runs_x) * nvy), rest = run - rz * (int64_t(runs_x) * nvy);
+    const int ry = int(rest / runs_x), rx = int(rest - int64_t(ry) * runs_x);
+    const int vx0 = P.vlo[0] + rx * PW, vy = P.vlo[1] + ry, vz = P.vlo[2] + int(rz);
+    const int npat = min(PW, P.vlo[0] + nvx - vx0);
+    const int vx = vx0 + p;
+    const bool live = lane < LY::LANES && p < npat;
+    const int varx = variant_of(vx, N), vary = variant_of(vy, N), varz = variant_of(vz, N);
+    const bool inner = vary == 1 && varz == 1 && vx0 > 1 && vx0 + npat - 1 < N - 1;   // uniform over the warp
+    const int64_t g0 = ((int64_t(vz - 1) * K + m - P.row0) * n + int64_t(vy - 1) * K) * n + int64_t(vx - 1) * K;
+    T pl[NP][NP];                                  // [y row j][x column i] of plane m
+#pragma unroll
+    for (int j = 0; j < NP; ++j)
+#pragma unroll
+      for (int i = 0; i < NP; ++i) pl[j][i] = live ? P.r[g0 + int64_t(j) * n + i] : T(0);
+    auto body = [&](auto INC) {
+      constexpr bool IN = decltype(INC)::value;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      auto Sx = [&](int idx) { return IN ? c.S[1][idx] : sS[varx * NP2 + idx]; };
+      auto Sy = [&](int idx) { return IN ? c.S[1][idx] : sS[vary * NP2 + idx]; };
+      auto Sz = [&](int idx) { return IN ? c.S[1][idx] : sS[varz * NP2 + idx]; };
+      T w[NP], o[NP];
+      // S_x^T along the rows, S_y^T along the columns (registers)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) w[i] = pl[j][i];
+        line_mul<NP, true>(Sx, w, o);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) pl[j][i] = o[i];
+      }
+#pragma unroll
+      for (int i = 0; i < NP; ++i) {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) w[j] = pl[j][i];
+        line_mul<NP, true>(Sy, w, o);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) pl[j][i] = o[j];
+      }
+      // transpose: lane (p, m) now takes the z lines q = m + NP t of patch p (lanes >= LANES hold no plane)
+      if (lane < LY::LANES) {
+#pragma unroll
+        for (int j = 0; j < NP; ++j)
+#pragma unroll
+          for (int i = 0; i < NP; ++i) buf[lane * PL + j * NP + i] = pl[j][i];
+      }
+      __syncwarp();
+      if (lane < LY::LANES) {
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+          const int q = m + NP * t;                 // line (j, i) = (q / NP, q % NP)
+#pragma unroll
+          for (int mm = 0; mm < NP; ++mm) w[mm] = buf[(p * NP + mm) * PL + q];
+          line_mul<NP, true>(Sz, w, o);
+          if (IN) {
+#pragma unroll
+            for (int mm = 0; mm < NP; ++mm) o[mm] *= tab[mm * NP2 + q];
+          } else {
+            const int qj = q / NP, qi = q - qj * NP;
+            const T lxy = sL[varx * NP + qi] + sL[vary * NP + qj];
+#pragma unroll
+            for (int mm = 0; mm < NP; ++mm) o[mm] /= (lxy + sL[varz * NP + mm]);
+          }
+          line_mul<NP, false>(Sz, o, w);
+#pragma unroll
+          for (int mm = 0; mm < NP; ++mm) buf[(p * NP + mm) * PL + q] = w[mm];
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < NP; ++j)
+#pragma unroll
+        for (int i = 0; i < NP; ++i) pl[j][i] = lane < LY::LANES ? buf[lane * PL + j * NP + i] : T(0);
+      __syncwarp();                                 // the buffer is rewritten by the next run
+      // S_y along the columns, S_x along the rows
+#pragma unroll
+      for (int i = 0; i < NP; ++i) {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) w[j] = pl[j][i];
+        line_mul<NP, false>(Sy, w, o);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) pl[j][i] = o[j];
+      }
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) w[i] = pl[j][i];
+        line_mul<NP, false>(Sx, w, o);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) pl[j][i] = o[i];
+      }
+    };
+    if (inner) body(std::true_type{});
+    else body(std::false_type{});
+    // run merge: columns [0, K-1) of patch p + 1 are columns [K, 2K-1) of patch p
+#pragma unroll
+    for (int cc = 0; cc < K - 1; ++cc)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        const T v = __shfl_down_sync(0xffffffffu, pl[j][cc], NP);
+        if (p + 1 < npat) pl[j][K + cc] += v;
+      }
+    const int64_t jz = int64_t(vz - 1) * K + 1 + m;
+    if (live && jz >= P.out_lo && jz < P.out_hi) {
+      const int c0 = p > 0 ? K - 1 : 0;
+#pragma unroll
+      for (int j = 0; j < NP; ++j)
+#pragma unroll
+        for (int i = 0; i < NP; ++i)
+          if (i >= c0) atomicAdd(P.x + g0 + int64_t(j) * n + i, P.factor * pl[j][i]);
+    }
+  }
+}
+
 // ----------------------------------------------------------------------------- patch_fdm3d_zrun
 // Deterministic additive FDM update without atomics: one warp per patch column (vx, vy) of one x-y
 // parity class (columns of a class are disjoint in x and y), walking the patches of the column along
@@ -1354,6 +1525,27 @@ static void launch_fdm3(const FusedLevel& F, T omega, const T* r, T* x, const Pa
   if (!atomic) {                 // disjoint list: CTA-cooperative kernel (measured faster)
     launch_fdm3_cta<T, K>(p, ps.count, st);
     return;
+  }
+  if constexpr (K <= 3) {
+    // atomic AVS over a box of vertices: runs of patches along x (patch_fdm3d_run_kernel)
+    if (!ps.list && ps.vstr == 1 && !std::getenv("C0IP_FDM3_NORUN")) {
+      using RL = Fdm3RunLayout<T, K>;
+      const size_t rsm = sizeof(T) * size_t(RL::TOTAL);
+      static int rgrid = -1;
+      if (rgrid < 0) {
+        cudaFuncSetAttribute(patch_fdm3d_run_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+        cudaFuncSetAttribute(patch_fdm3d_run_kernel<T, K>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        int dev = 0, sms = 148, per = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, patch_fdm3d_run_kernel<T, K>, 256, rsm);
+        rgrid = sms * std::max(per, 1);
+      }
+      const int64_t runs = int64_t((ps.vcnt[0] + RL::PW - 1) / RL::PW) * ps.vcnt[1] * ps.vcnt[2];
+      const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(rgrid, (runs + 7) / 8));
+      patch_fdm3d_run_kernel<T, K><<<(unsigned)grid, 256, rsm, st>>>(p);
+      return;
+    }
   }
   static int grid_cache = -1;
   if (grid_cache < 0) {

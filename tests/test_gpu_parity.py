@@ -424,7 +424,7 @@ def test_slab_rejects_missing_ghosts():
 
 
 # ------------------------------------------------------------------------------ 3D fused kernels (N >= 8)
-CASES_3D_FUSED = [(3, 2, 8), (3, 3, 9), (3, 4, 8), (3, 5, 8), (3, 3, 10), (3, 2, 12)]
+CASES_3D_FUSED = [(3, 2, 8), (3, 3, 9), (3, 4, 8), (3, 5, 8), (3, 3, 10), (3, 2, 12), (3, 2, 16)]
 
 
 @pytest.mark.parametrize("d,k,N", CASES_3D_FUSED)
