@@ -459,6 +459,9 @@ void disjoint_patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, con
       c0ip::fused3_patch_fdm<T>(*L.fused, omega, r, x, list, count, st, &ctx->launches))
     return;
   if (mma_patches<T>(ctx, L, r, x, omega, list, count, 0, st)) return;
+  if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 2 &&
+      c0ip::fused2_patch_list<T>(*L.fused, omega, r, x, list, count, st, &ctx->launches))
+    return;
   patch_solve<T>(ctx, L, r, x, omega, list, count, 0, st);
 }
 

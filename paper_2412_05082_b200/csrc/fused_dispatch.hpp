@@ -42,6 +42,11 @@ template <typename T>
 bool fused_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega, const T* b, T* x,
                      cudaStream_t st, int64_t* launches);
 
+// 2D: x += omega A~_v^{-1} R_v r over a list of mutually disjoint patches (one MVS colour, k >= 5)
+template <typename T>
+bool fused2_patch_list(FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
+                       cudaStream_t st, int64_t* launches);
+
 // 3D (fused3d.cu): matvec / residual, and the per-patch FDM update x += omega A~_v^{-1} R_v r over a
 // list of mutually disjoint patches (a parity class or a colour)
 template <typename T>

@@ -1222,11 +1222,207 @@ static void launch_mvs(const FusedLevel& F, const int32_t* list, int64_t count, 
   mvs2d_kernel<T, K><<<(unsigned)grid, 256, smem, st>>>(p);
 }
 
+// ----------------------------------------------------------------------------- patch_list2d
+// x += omega h^2 A~_v^{-1} R_v r over a list of mutually disjoint patches (one MVS colour after a full
+// residual): NP = 2K - 1 lanes per patch, PW = 32 / NP patches per warp; lane
+// (p, j) loads row j of patch p and contracts it with S_x^T in registers, one transpose through a per-warp
+// shared buffer gives lane (p, i) the column i for S_y^T, the scaling 1 / (lam_x,i + lam_y,j) and S_y, a
+// second transpose returns the rows for S_x and the update (plain read-modify-write: the patches of the
+// list are disjoint).  Warps whose patches are all interior take S as warp-uniform kernel-parameter
+// operands, the others read the per-lane variants from a shared copy.  Used for the 2D MVS at k >= 5,
+// where the fused per-patch footprint residual (mvs2d_kernel) costs more than one residual per colour.
+template <typename T, int K>
+struct PatchListP {
+  Coef2<T, K> c;
+  const T* r;
+  T* x;
+  const int32_t* list;
+  int64_t count;
+  int64_t N, n;
+  T factor;                 // omega h^2
+  int zero;
+};
+
+template <typename T, int K>
+struct List2Layout {
+  static constexpr int NP = 2 * K - 1, NP2 = NP * NP, PW = 32 / NP, LANES = PW * NP;
+  static constexpr int PR = NP | 1;                // odd row pitch
+  static constexpr int WB = PW * NP * PR;          // per-warp buffer
+  static constexpr int TOTAL = 8 * WB + NP2 + 3 * NP2 + 3 * NP;   // | interior 1/(lx+ly) | S[3] | lam[3]
+};
+
+template <typename T, int K>
+__global__ void __launch_bounds__(256) patch_list2d_kernel(const __grid_constant__ PatchListP<T, K> P) {
+  using LY = List2Layout<T, K>;
+  constexpr int NP = LY::NP, NP2 = LY::NP2, PW = LY::PW, PR = LY::PR;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* const sm = reinterpret_cast<T*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  T* const buf = sm + warp * LY::WB;
+  T* const tab = sm + 8 * LY::WB;                  // [i][j] interior 1 / (lam_i + lam_j)
+  T* const sS = tab + NP2;
+  T* const sL = sS + 3 * NP2;
+  for (int e = tid; e < NP2; e += 256) tab[e] = T(1) / (P.c.lam[1][e / NP] + P.c.lam[1][e % NP]);
+  for (int e = tid; e < 3 * NP2; e += 256) sS[e] = P.c.S[e / NP2][e % NP2];
+  for (int e = tid; e < 3 * NP; e += 256) sL[e] = P.c.lam[e / NP][e % NP];
+  __syncthreads();
+  const int64_t N = P.N, n = P.n;
+  const int Nm1 = int(N - 1);
+  const int p = lane / NP, j = lane - (lane / NP) * NP;
+  const int64_t ngroups = (P.count + PW - 1) / PW, gstride = int64_t(gridDim.x) * 8;
+  int round = 0;
+#pragma unroll 1
+  for (int64_t g = int64_t(blockIdx.x) * 8 + warp; g < ngroups; g += gstride, ++round) {
+    const int64_t q = g * PW + p;
+    const bool live = lane < LY::LANES && q < P.count;
+    int vx = 1, vy = 1;
+    if (live) {
+      const int pid = P.list[q];
+      vy = 1 + pid / Nm1;
+      vx = 1 + (pid - (vy - 1) * Nm1);
+    }
+    const int varx = variant_of(vx, N), vary = variant_of(vy, N);
+    const bool inner = __all_sync(0xffffffffu, !live || (varx == 1 && vary == 1));
+    // row j of the patch: nodes ((vx-1)K + 1 + i, (vy-1)K + 1 + j), interior index (jy - 1) n + (jx - 1)
+    const int64_t g0 = (int64_t(vy - 1) * K + j) * n + int64_t(vx - 1) * K;
+    // the lines live in the per-warp buffer; each contraction walks its input index l at run time (one
+    // buffer load and NP coefficient loads per l), so only the NP accumulators are live
+    T* const row = buf + (p * NP + j) * PR;          // row j of patch p
+    T* const col = buf + p * NP * PR + j;            // column i = j of patch p (stride PR)
+    const bool act = lane < LY::LANES;
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < NP; ++i) row[i] = live ? P.r[g0 + i] : T(0);
+    }
+    T o[NP];
+    auto body = [&](auto INC) {
+      constexpr bool IN = decltype(INC)::value;
+      const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
+      const T* const Sx = IN ? c.S[1] : sS + varx * NP2;
+      const T* const Sy = IN ? c.S[1] : sS + vary * NP2;
+      // S_x^T on row j
+#pragma unroll
+      for (int i = 0; i < NP; ++i) o[i] = 0;
+#pragma unroll 1
+      for (int l = 0; l < NP; ++l) {
+        const T wl = act ? row[l] : T(0);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) o[i] = fma(Sx[l * NP + i], wl, o[i]);
+      }
+      if (act) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) row[i] = o[i];
+      }
+      __syncwarp();
+      // lane (p, j) now owns column i = j: S_y^T, scale 1 / (lam_x,i + lam_y,jj), S_y
+#pragma unroll
+      for (int jj = 0; jj < NP; ++jj) o[jj] = 0;
+#pragma unroll 1
+      for (int l = 0; l < NP; ++l) {
+        const T wl = act ? col[l * PR] : T(0);
+#pragma unroll
+        for (int jj = 0; jj < NP; ++jj) o[jj] = fma(Sy[l * NP + jj], wl, o[jj]);
+      }
+      if (IN) {
+#pragma unroll
+        for (int jj = 0; jj < NP; ++jj) o[jj] *= tab[j * NP + jj];
+      } else {
+        const T lx = sL[varx * NP + j];
+#pragma unroll
+        for (int jj = 0; jj < NP; ++jj) o[jj] /= (lx + sL[vary * NP + jj]);
+      }
+      if (act) {                                     // the column is this lane's own: no sync needed
+#pragma unroll
+        for (int jj = 0; jj < NP; ++jj) col[jj * PR] = o[jj];
+      }
+#pragma unroll
+      for (int jj = 0; jj < NP; ++jj) o[jj] = 0;
+#pragma unroll 1
+      for (int l = 0; l < NP; ++l) {
+        const T wl = act ? col[l * PR] : T(0);
+#pragma unroll
+        for (int jj = 0; jj < NP; ++jj) o[jj] = fma(Sy[jj * NP + l], wl, o[jj]);
+      }
+      if (act) {
+#pragma unroll
+        for (int jj = 0; jj < NP; ++jj) col[jj * PR] = o[jj];
+      }
+      __syncwarp();
+      // S_x on row j
+#pragma unroll
+      for (int i = 0; i < NP; ++i) o[i] = 0;
+#pragma unroll 1
+      for (int l = 0; l < NP; ++l) {
+        const T wl = act ? row[l] : T(0);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) o[i] = fma(Sx[i * NP + l], wl, o[i]);
+      }
+      __syncwarp();                                  // the buffer is rewritten by the next group
+    };
+    if (inner) body(std::true_type{});
+    else body(std::false_type{});
+    if (live) {
+#pragma unroll
+      for (int i = 0; i < NP; ++i) P.x[g0 + i] = fma(P.factor, o[i], P.x[g0 + i]);
+    }
+  }
+}
+
+template <typename T, int K>
+static void launch_list2d(const FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
+                          cudaStream_t st) {
+  using LY = List2Layout<T, K>;
+  const size_t smem = sizeof(T) * size_t(LY::TOTAL);
+  static int grid_cache = -1;
+  if (grid_cache < 0) {
+    cudaFuncSetAttribute(patch_list2d_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    grid_cache = persistent_grid(patch_list2d_kernel<T, K>, smem, 1 << 30);
+  }
+  PatchListP<T, K> p;
+  std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
+  p.r = r; p.x = x; p.list = list; p.count = count; p.N = F.N; p.n = F.n;
+  p.factor = T(double(omega) * F.h * F.h);
+  p.zero = 0;
+  const int64_t groups = (count + LY::PW - 1) / LY::PW;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(grid_cache, (groups + 7) / 8));
+  patch_list2d_kernel<T, K><<<(unsigned)grid, 256, smem, st>>>(p);
+}
+
+// lowest degree at which the 2D MVS colour runs as residual + patch_list2d instead of the fused
+// per-patch kernels (C0IP_MVS2D_SPLIT_K overrides: measurement knob)
+static int mvs2d_split_k() {
+  static const int k = [] {
+    const char* e = std::getenv("C0IP_MVS2D_SPLIT_K");
+    return e ? std::atoi(e) : 5;
+  }();
+  return k;
+}
+
+template <typename T>
+bool fused2_patch_list(FusedLevel& F, T omega, const T* r, T* x, const int32_t* list, int64_t count,
+                       cudaStream_t st, int64_t* launches) {
+  if (F.d != 2) return false;
+  if (count == 0) return true;
+  switch (F.k) {
+    case 2: launch_list2d<T, 2>(F, omega, r, x, list, count, st); break;
+    case 3: launch_list2d<T, 3>(F, omega, r, x, list, count, st); break;
+    case 4: launch_list2d<T, 4>(F, omega, r, x, list, count, st); break;
+    case 5: launch_list2d<T, 5>(F, omega, r, x, list, count, st); break;
+    case 6: launch_list2d<T, 6>(F, omega, r, x, list, count, st); break;
+    case 7: launch_list2d<T, 7>(F, omega, r, x, list, count, st); break;
+    default: return false;
+  }
+  (*launches)++;
+  check_launch("patch_list2d launch");
+  return true;
+}
+
 template <typename T>
 bool fused_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega, const T* b, T* x, cudaStream_t st,
                      int64_t* launches) {
   if (F.d != 2) return false;
   if (count == 0) return true;
+  if (F.k >= mvs2d_split_k()) return false;     // caller: residual + fused2_patch_list per colour
   if constexpr (std::is_same<T, double>::value) {
     if (mma_mvs2d(F, list, count, double(omega), b, x, st)) {
       (*launches)++;
@@ -1255,7 +1451,8 @@ int fused_dim(const FusedLevel& F) { return F.d; }
   template bool fused_apply<T>(FusedLevel&, const T*, const T*, T*, cudaStream_t, int64_t*, const SlabWindow*); \
   template bool fused_fdm<T>(FusedLevel&, T, const T*, T*, cudaStream_t, int64_t*, const SlabWindow*);        \
   template bool fused_avs<T>(FusedLevel&, T, const T*, T*, T*, cudaStream_t, int64_t*);                        \
-  template bool fused_mvs_color<T>(FusedLevel&, const int32_t*, int64_t, T, const T*, T*, cudaStream_t, int64_t*);
+  template bool fused_mvs_color<T>(FusedLevel&, const int32_t*, int64_t, T, const T*, T*, cudaStream_t, int64_t*); \
+  template bool fused2_patch_list<T>(FusedLevel&, T, const T*, T*, const int32_t*, int64_t, cudaStream_t, int64_t*);
 C0IP_INST(double)
 C0IP_INST(float)
 #undef C0IP_INST
