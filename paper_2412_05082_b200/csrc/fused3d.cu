@@ -76,30 +76,33 @@ __device__ __forceinline__ T row_band(F coef, const T* w, int base) {
 
 // K node planes z0 .. z0+K-1 of the in-plane box into smem (cp.async, zero fill outside the domain)
 // (node plane jz lives at local plane jz - 1 - row0, valid for local planes [0, lrows)).  Thread t copies
-// elements t, t + 256, ... of the K x BW x BW box: the element -> (plane, row, column) split is by
-// compile-time constants and the 64-bit base address is formed once per call, so a box that lies inside
+// the in-plane positions t, t + 256, ... of the BW x BW box for all K planes: one split of the position
+// by a compile-time constant per position, the 64-bit base address formed once per call, so a box inside
 // the domain (every CTA but the boundary ones) costs a few integer instructions per element.
 template <typename T, int K, int BW, int PX>
 __device__ __forceinline__ void load_planes_async(T* dst, const T* src, int64_t n, int64_t KN, int64_t z0,
                                                   int64_t Y0, int64_t X0, int64_t row0, int64_t lrows) {
-  constexpr int TOT = K * BW * BW;
+  constexpr int TOT2 = BW * BW;
   const int64_t zlo = (row0 + 1 > 1) ? row0 + 1 : int64_t(1), zhi = (row0 + lrows < KN - 1) ? row0 + lrows : KN - 1;
   const bool inner = (X0 >= 1 && X0 + BW - 1 <= KN - 1 && Y0 >= 1 && Y0 + BW - 1 <= KN - 1 && z0 >= zlo &&
                       z0 + K - 1 <= zhi);
   const T* base = src + ((z0 - 1 - row0) * n + (Y0 - 1)) * n + (X0 - 1);
-  const int nn = int(n);
-  if (inner) {
-#pragma unroll 4
-    for (int e = threadIdx.x; e < TOT; e += 256) {
-      const int pz = e / (BW * BW), rc = e - pz * (BW * BW), r = rc / BW, cc = rc - r * BW;
-      cp_async_elem(dst + (pz * BW + r) * PX + cc, base + ((int64_t)pz * nn + r) * nn + cc, true);
-    }
-  } else {
-    for (int e = threadIdx.x; e < TOT; e += 256) {
-      const int pz = e / (BW * BW), rc = e - pz * (BW * BW), r = rc / BW, cc = rc - r * BW;
-      const int64_t jz = z0 + pz, jy = Y0 + r, jx = X0 + cc;
-      const bool ok = jz >= zlo && jz <= zhi && jy >= 1 && jy <= KN - 1 && jx >= 1 && jx <= KN - 1;
-      cp_async_elem(dst + (pz * BW + r) * PX + cc, ok ? base + ((int64_t)pz * nn + r) * nn + cc : src, ok);
+  const int64_t pstride = n * n;
+  for (int rc = threadIdx.x; rc < TOT2; rc += 256) {
+    const int r = rc / BW, cc = rc - r * BW;
+    T* const d = dst + r * PX + cc;
+    const T* const s0 = base + int64_t(r) * n + cc;
+    if (inner) {
+#pragma unroll
+      for (int pz = 0; pz < K; ++pz) cp_async_elem(d + pz * (BW * PX), s0 + pz * pstride, true);
+    } else {
+      const int64_t jy = Y0 + r, jx = X0 + cc;
+      const bool xy = jy >= 1 && jy <= KN - 1 && jx >= 1 && jx <= KN - 1;
+#pragma unroll
+      for (int pz = 0; pz < K; ++pz) {
+        const bool ok = xy && z0 + pz >= zlo && z0 + pz <= zhi;
+        cp_async_elem(d + pz * (BW * PX), ok ? s0 + pz * pstride : src, ok);
+      }
     }
   }
 }
@@ -713,7 +716,7 @@ __global__ void __launch_bounds__(256, (K == 3 && sizeof(T) == 8) ? 3 : 4) patch
   }
 }
 
-// ----------------------------------------------------------------------------- patch_fdm3d_run (k <= 3)
+// ----------------------------------------------------------------------------- patch_fdm3d_run
 // Atomic AVS patch solves x += omega h A~_v^{-1} R_v r for runs of PW consecutive
 // patches along x (same vy, vz): NP = 2K - 1 lanes per patch, PW = 32 / NP patches per warp; lane (p, m)
 // holds the node plane z = m of patch p (NP x NP values in registers).  S_x^T and S_y^T (and S_y, S_x on the
@@ -723,7 +726,8 @@ __global__ void __launch_bounds__(256, (K == 3 && sizeof(T) == 8) ? 3 : 4) patch
 // (p + 1, m) hands those columns to lane (p, m) (warp shuffles), which adds them before its red.global.add,
 // so the run updates every node column once per plane ((2k-1)/k instead of ((2k-1)/k)^3 atomics per DoF
 // along x).  Interior runs take coefficients as warp-uniform kernel-parameter operands; runs touching the
-// boundary read per-lane variants from a shared copy.
+// boundary read per-lane variants from a shared copy.  Used for k <= 3 (2 CTAs per SM); at k = 4 the 49
+// plane values per lane leave 1 CTA per SM and the kernel measured no faster than patch_fdm3d_kernel.
 template <typename T, int K>
 struct Fdm3RunLayout {
   static constexpr int NP = 2 * K - 1, NP2 = NP * NP, PW = 32 / NP, LANES = PW * NP;
@@ -745,7 +749,7 @@ __device__ __forceinline__ void line_mul(F coef, const T (&w)[NP], T (&o)[NP]) {
 }
 
 template <typename T, int K>
-__global__ void __launch_bounds__(256, 2) patch_fdm3d_run_kernel(const __grid_constant__ Fdm3P<T, K> P) {
+__global__ void __launch_bounds__(256, K <= 3 ? 2 : 1) patch_fdm3d_run_kernel(const __grid_constant__ Fdm3P<T, K> P) {
   using LY = Fdm3RunLayout<T, K>;
   constexpr int NP = LY::NP, NP2 = LY::NP2, PW = LY::PW, PL = LY::PL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1526,7 +1530,7 @@ static void launch_fdm3(const FusedLevel& F, T omega, const T* r, T* x, const Pa
     launch_fdm3_cta<T, K>(p, ps.count, st);
     return;
   }
-  if constexpr (K <= 3) {
+  if constexpr (K <= 3) {   // k = 4: 3.35 vs 3.26 ms for the warp-per-patch kernel (1 CTA/SM at 253 registers)
     // atomic AVS over a box of vertices: runs of patches along x (patch_fdm3d_run_kernel)
     if (!ps.list && ps.vstr == 1 && !std::getenv("C0IP_FDM3_NORUN")) {
       using RL = Fdm3RunLayout<T, K>;
