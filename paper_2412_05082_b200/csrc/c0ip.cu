@@ -1576,11 +1576,18 @@ void slab_mvs_color_impl(c0ip_ctx ctx, Level& L, int color, T omega, int64_t row
   // the same kernel as the single-domain step (fused apply3d on the window, else the generic per-axis kernels)
   const int64_t KN = int64_t(k) * L.N;
   const c0ip::SlabWindow wr{row0, lrows, std::max<int64_t>(1, out_lo - (k - 1)), std::min<int64_t>(KN, out_hi + k)};
-  if (!(ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
-        c0ip::fused3_apply<T>(*L.fused, x_ext, b_ext, r_ext, st, &ctx->launches, &wr)))
+  const bool fused = ctx->path == C0IP_PATH_AUTO && L.fused;
+  if (!(fused && c0ip::fused_dim(*L.fused) == 3 &&
+        c0ip::fused3_apply<T>(*L.fused, x_ext, b_ext, r_ext, st, &ctx->launches, &wr)) &&
+      !(fused && c0ip::fused_dim(*L.fused) == 2 &&
+        c0ip::fused_apply<T>(*L.fused, x_ext, b_ext, r_ext, st, &ctx->launches, &wr)))
     generic_apply<T>(ctx, L, xv, bv, rv, st, wr.out_lo - 1, wr.out_hi - 1);
   if (ctx->local == C0IP_LOCAL_EXACT) throw std::runtime_error("slab MVS with exact local solvers is not supported");
   if (mma_patches<T>(ctx, L, rv, xv, omega, list, cnt, 0, st)) return;
+  // 2D k >= 5 (and FP32): the kernel of the single-domain colour step, so the owned rows stay bitwise equal
+  if (fused && c0ip::fused_dim(*L.fused) == 2 &&
+      c0ip::fused2_patch_list<T>(*L.fused, omega, rv, xv, list, cnt, st, &ctx->launches))
+    return;
   if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
       c0ip::fused3_patch_fdm<T>(*L.fused, omega, rv, xv, list, cnt, st, &ctx->launches, 0))
     return;

@@ -1106,14 +1106,15 @@ static void launch_apply_nt(const FusedLevel& F, const T* x, const T* b, T* y, c
   apply2d_kernel<T, K, NT><<<grid, NT, smem, st>>>(p);
 }
 
-// CTA size: 128 threads where the register-blocked column-walk stages have ~128 units (FP64 k = 4),
-// 256 otherwise; C0IP_APPLY_NT overrides (measurement knob)
+// CTA size: 128 threads for FP64 (the column-walk stages have ~128 register-blocked units at k = 4; measured
+// residual k = 2..7 0.158/0.206/0.162/0.242/0.332/0.364 ms vs 0.158/0.214/0.192/0.280/0.315/0.423 ms with
+// 256 threads), except k = 6; 256 for FP32; C0IP_APPLY_NT overrides (measurement knob)
 template <typename T, int K>
 static void launch_apply(const FusedLevel& F, const T* x, const T* b, T* y, const SlabWindow& w, cudaStream_t st) {
   static const int nt = [] {
     const char* e = std::getenv("C0IP_APPLY_NT");
     if (e) return std::atoi(e) == 128 ? 128 : 256;
-    return (K == 4 && sizeof(T) == 8) ? 128 : 256;
+    return (sizeof(T) == 8 && K != 6) ? 128 : 256;
   }();
   if (nt == 128) launch_apply_nt<T, K, 128>(F, x, b, y, w, st);
   else launch_apply_nt<T, K, 256>(F, x, b, y, w, st);
