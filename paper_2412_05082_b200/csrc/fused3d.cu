@@ -53,7 +53,9 @@ template <typename T, int K>
 struct Apply3Layout {
   static constexpr int C = Tile3<K>::C, O = Tile3<K>::O;
   static constexpr int BW = (C + 3) * K + 1;      // in-plane box [(c0-2)K, (c0+C+1)K]
-  static constexpr int PX = odd(BW), PO = odd(O);
+  // x-stage output pitch odd and >= O + 1: with the y-stage columns padded to OP = 16 lanes per cell row (O = 15
+  // at k = 3, 5) the two half-warps cover every bank pair once (PO = 15 gave 3-way conflicts on the column loads)
+  static constexpr int PX = odd(BW), PO = odd(O + 1), OP = (O == 15) ? 16 : O;
   static constexpr int XB = K * BW * PX;          // K planes of the box (double buffered)
   static constexpr int SX = K * 3 * BW * PO;      // x-stage outputs (B, L, M) of K planes
   static constexpr int PQR = K * 3 * O * O;       // in-plane results of K planes
@@ -211,11 +213,12 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
 
     // y-stage: unit = (plane, owned column, cell row) -> P, Q, R for the K nodes of the cell row
 #pragma unroll 1
-    for (int it = 0; it < cdiv(K * O * C, NT); ++it, ++round) {
+    for (int it = 0; it < cdiv(K * LY::OP * C, NT); ++it, ++round) {
       const int u = it * NT + tid;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
-      if (u >= K * O * C) continue;
-      const int col = u % O, rest = u / O, ci = rest % C, pz = rest / C;
+      if (u >= K * LY::OP * C) continue;
+      const int col = u % LY::OP, rest = u / LY::OP, ci = rest % C, pz = rest / C;
+      if (col >= O) continue;
       const int64_t cy = cy0 + ci;
       if (cy >= N) continue;
       const T* sB = sx + (pz * 3 + 0) * BW * PO;
