@@ -124,6 +124,8 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
   const int tile = blockIdx.x % (ntx * ntx), chunk = blockIdx.x / (ntx * ntx);
   const int64_t cx0 = int64_t(tile % ntx) * C, cy0 = int64_t(tile / ntx) * C, cz0 = P.cz_lo + int64_t(chunk) * CZ;
   const int tid = threadIdx.x;
+  // tiles whose cells are all interior along x / y take the all-classes interior rows (CTA-uniform)
+  const bool tinx = (cx0 >= 2 && cx0 + C - 1 <= N - 2), tiny = (cy0 >= 2 && cy0 + C - 1 <= N - 2);
   const int oy = tid / O, ox = tid - (tid / O) * O;       // z-stage ownership (tid < O*O)
   const bool zown = tid < O * O;
   // z-stage, two forms (measured per degree):
@@ -179,6 +181,21 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
         for (int j = 0; j < XR; ++j)
 #pragma unroll
           for (int q = 0; q <= 4 * K; ++q) w[j][q] = xb[(pz * BW + rr[j]) * PX + ci * K + q];
+        if (tinx) {                 // every cell of the tile interior along x: all K classes at once
+          T ob[K][XR], ol[K][XR], om[K][XR];
+          x_all_interior<T, K, XR>(c, w, ob, ol, om);
+#pragma unroll
+          for (int p = 0; p < K; ++p)
+#pragma unroll
+            for (int j = 0; j < XR; ++j) {
+              if (hr + j * HB >= BW) continue;
+              const int r = rr[j];
+              sx[((pz * 3 + 0) * BW + r) * PO + ci * K + p] = ob[p][j];
+              sx[((pz * 3 + 1) * BW + r) * PO + ci * K + p] = ol[p][j];
+              sx[((pz * 3 + 2) * BW + r) * PO + ci * K + p] = om[p][j];
+            }
+          continue;
+        }
         const bool inner = (cx >= 2 && cx <= N - 2);
 #pragma unroll
         for (int p = 0; p < K; ++p) {
@@ -231,6 +248,30 @@ __global__ void __launch_bounds__(256, Apply3Layout<T, K>::MINB) apply3d_kernel(
       for (int q = 0; q <= 2 * K; ++q) {
         wB[q] = sB[(ci * K + K + q) * PO + col];
         wL[q] = sL[(ci * K + K + q) * PO + col];
+      }
+      if (tiny) {                   // every cell row of the tile interior along y: all K classes at once
+        T w1[1][4 * K + 1], wb[1][2 * K + 1], wl[1][2 * K + 1], wmk[1][2 * K + 1];
+#pragma unroll
+        for (int q = 0; q <= 4 * K; ++q) w1[0][q] = wM[q];
+#pragma unroll
+        for (int q = 0; q <= 2 * K; ++q) { wb[0][q] = wB[q]; wl[0][q] = wL[q]; wmk[0][q] = wM[K + q]; }
+        T aP[K][1], aL[K][1], aQ[K][1], aR[K][1];
+#pragma unroll
+        for (int p = 0; p < K; ++p) aP[p][0] = aL[p][0] = aQ[p][0] = aR[p][0] = T(0);
+        y_all_interior<T, K, 1, 0, 4 * K + 1>(c, w1, aP);     // B^_y (M^_x x)
+        y_all_interior<T, K, 1, 1, 2 * K + 1>(c, wb, aP);     // M^_y (B^_x x)
+        y_all_interior<T, K, 1, 2, 2 * K + 1>(c, wl, aL);     // L^_y (L^_x x)
+        y_all_interior<T, K, 1, 2, 2 * K + 1>(c, wmk, aQ);    // L^_y (M^_x x)
+        y_all_interior<T, K, 1, 1, 2 * K + 1>(c, wl, aQ);     // M^_y (L^_x x)
+        y_all_interior<T, K, 1, 1, 2 * K + 1>(c, wmk, aR);    // M^_y (M^_x x)
+#pragma unroll
+        for (int p = 0; p < K; ++p) {
+          const int orow = ci * K + p;
+          pqr[((pz * 3 + 0) * O + orow) * O + col] = fma(T(2), aL[p][0], aP[p][0]);
+          pqr[((pz * 3 + 1) * O + orow) * O + col] = aQ[p][0];
+          pqr[((pz * 3 + 2) * O + orow) * O + col] = aR[p][0];
+        }
+        continue;
       }
       const bool inner = (cy >= 2 && cy <= N - 2);
 #pragma unroll

@@ -135,6 +135,69 @@ __device__ __forceinline__ void rowML(F coef, const T (&w)[RB][W], int wofs, T (
   }
 }
 
+// ----------------------------------------------------------------------------- interior rows, all classes
+// acc[r] += c * w[r][o] over the RB lines of a thread; FP32 pairs go through the packed FFMA2 (f32x2
+// FMA with a scalar uniform operand on sm_100a: two FMAs per issue slot)
+template <typename T, int RB, int W>
+__device__ __forceinline__ void fma_rb(T c, const T (&w)[RB][W], int o, T (&acc)[RB]) {
+  if constexpr (std::is_same<T, float>::value && RB >= 2) {
+#pragma unroll
+    for (int r = 0; r + 1 < RB; r += 2) {
+      const float2 v = __ffma2_rn(make_float2(c, c), make_float2(w[r][o], w[r + 1][o]),
+                                  make_float2(acc[r], acc[r + 1]));
+      acc[r] = v.x;
+      acc[r + 1] = v.y;
+    }
+    if constexpr (RB % 2 == 1) acc[RB - 1] = fmaf(c, w[RB - 1][o], acc[RB - 1]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[r] = fma(c, w[r][o], acc[r]);
+  }
+}
+
+// Interior rows of all K classes of one cell at once, window index outermost so that every DFMA
+// of an accumulator is separated by the other 3K*RB (or K*RB) accumulators (ILP), coefficients
+// shared by the RB lines.  w[r][o] <-> node (c-2)K + o.
+template <typename T, int K, int RB>
+__device__ __forceinline__ void x_all_interior(const Coef2<T, K>& c, const T (&w)[RB][4 * K + 1], T (&ob)[K][RB],
+                                               T (&ol)[K][RB], T (&om)[K][RB]) {
+#pragma unroll
+  for (int p = 0; p < K; ++p)
+#pragma unroll
+    for (int r = 0; r < RB; ++r) ob[p][r] = ol[p][r] = om[p][r] = 0;
+#pragma unroll
+  for (int o = 0; o <= 4 * K; ++o)
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      const int q = o - p;                           // B coefficient index (offset q - 2K)
+      if (q >= 0 && q <= 4 * K && (p == 0 || (q >= K - p && q <= 4 * K - p))) {
+        fma_rb<T, RB>(c.BI[p][q], w, o, ob[p]);
+      }
+      const int qm = o - p - K;                      // M/L coefficient index (offset qm - K)
+      if (qm >= 0 && qm <= 2 * K && (p == 0 || (qm >= K - p && qm <= 2 * K - p))) {
+        fma_rb<T, RB>(c.LI[p][qm], w, o, ol[p]);
+        fma_rb<T, RB>(c.MI[p][qm], w, o, om[p]);
+      }
+    }
+}
+
+// acc[p][r] += sum over the band of class p: WHICH 0 = B (window 4K+1, base (c-2)K), 1 = M, 2 = L
+// (window 2K+1, base (c-1)K); window index outermost.
+template <typename T, int K, int RB, int WHICH, int W>
+__device__ __forceinline__ void y_all_interior(const Coef2<T, K>& c, const T (&w)[RB][W], T (&acc)[K][RB]) {
+#pragma unroll
+  for (int o = 0; o < W; ++o)
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      const int q = o - p;
+      const bool ok = (WHICH == 0) ? (q >= 0 && q <= 4 * K && (p == 0 || (q >= K - p && q <= 4 * K - p)))
+                                   : (q >= 0 && q <= 2 * K && (p == 0 || (q >= K - p && q <= 2 * K - p)));
+      if (ok) {
+        fma_rb<T, RB>((WHICH == 0) ? c.BI[p][q] : (WHICH == 1 ? c.MI[p][q] : c.LI[p][q]), w, o, acc[p]);
+      }
+    }
+}
+
 // ----------------------------------------------------------------------------- async copies
 // cp.async (LDGSTS) element copies global -> shared with zero fill (src-size 0) for the nodes
 // outside the interior (the eliminated clamped-boundary nodes).
