@@ -507,7 +507,9 @@ def _sample_ids(n, d, rng, m=48):
 
 
 @pytest.mark.parametrize("d,k,sm", [(2, 4, "avs_atomic"), (2, 4, "avs"), (2, 3, "avs_atomic"), (2, 2, "avs_atomic"),
-                                    (3, 3, "avs_atomic"), (3, 2, "avs"), (3, 4, "avs_atomic"), (3, 5, "avs_atomic")])
+                                    (2, 5, "avs"), (2, 7, "avs"),
+                                    (3, 3, "avs_atomic"), (3, 2, "avs_atomic"), (3, 2, "avs"), (3, 4, "avs_atomic"),
+                                    (3, 5, "avs_atomic")])
 def test_full_size_sampled_avs(d, k, sm):
     from c0ip_inputs import CFG2_CELLS, CFG4_CELLS
     from oracle.smoothers import avs_delta_sample
