@@ -1167,8 +1167,9 @@ static void launch_mvs(const FusedLevel& F, const int32_t* list, int64_t count, 
 // (p, j) loads row j of patch p and contracts it with S_x^T in registers, one transpose through a per-warp
 // shared buffer gives lane (p, i) the column i for S_y^T, the scaling 1 / (lam_x,i + lam_y,j) and S_y, a
 // second transpose returns the rows for S_x and the update (plain read-modify-write: the patches of the
-// list are disjoint).  Warps whose patches are all interior take S as warp-uniform kernel-parameter
-// operands, the others read the per-lane variants from a shared copy.  Used for the 2D MVS at k >= 5,
+// list are disjoint).  Each lane holds the row of G = 2 patches (two groups per warp iteration) so that a
+// coefficient load serves two lines.  Warps whose patches are all interior take S as warp-uniform
+// kernel-parameter operands, the others read the per-lane variants from a shared copy.  Used for the 2D MVS at k >= 5,
 // where the fused per-patch footprint residual (mvs2d_kernel) costs more than one residual per colour.
 template <typename T, int K>
 struct PatchListP {
@@ -1185,15 +1186,17 @@ struct PatchListP {
 template <typename T, int K>
 struct List2Layout {
   static constexpr int NP = 2 * K - 1, NP2 = NP * NP, PW = 32 / NP, LANES = PW * NP;
+  static constexpr int G = 2;                      // patch groups per warp iteration (coefficient reuse)
   static constexpr int PR = NP | 1;                // odd row pitch
-  static constexpr int WB = PW * NP * PR;          // per-warp buffer
+  static constexpr int GB = PW * NP * PR;          // one group's buffer
+  static constexpr int WB = G * GB;                // per-warp buffer
   static constexpr int TOTAL = 8 * WB + NP2 + 3 * NP2 + 3 * NP;   // | interior 1/(lx+ly) | S[3] | lam[3]
 };
 
 template <typename T, int K>
 __global__ void __launch_bounds__(256) patch_list2d_kernel(const __grid_constant__ PatchListP<T, K> P) {
   using LY = List2Layout<T, K>;
-  constexpr int NP = LY::NP, NP2 = LY::NP2, PW = LY::PW, PR = LY::PR;
+  constexpr int NP = LY::NP, NP2 = LY::NP2, PW = LY::PW, PR = LY::PR, G = LY::G;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* const sm = reinterpret_cast<T*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1208,102 +1211,129 @@ __global__ void __launch_bounds__(256) patch_list2d_kernel(const __grid_constant
   const int64_t N = P.N, n = P.n;
   const int Nm1 = int(N - 1);
   const int p = lane / NP, j = lane - (lane / NP) * NP;
-  const int64_t ngroups = (P.count + PW - 1) / PW, gstride = int64_t(gridDim.x) * 8;
+  const bool act = lane < LY::LANES;
+  const int64_t ngroups = (P.count + G * PW - 1) / (G * PW), gstride = int64_t(gridDim.x) * 8;
   int round = 0;
 #pragma unroll 1
   for (int64_t g = int64_t(blockIdx.x) * 8 + warp; g < ngroups; g += gstride, ++round) {
-    const int64_t q = g * PW + p;
-    const bool live = lane < LY::LANES && q < P.count;
-    int vx = 1, vy = 1;
-    if (live) {
-      const int pid = P.list[q];
-      vy = 1 + pid / Nm1;
-      vx = 1 + (pid - (vy - 1) * Nm1);
-    }
-    const int varx = variant_of(vx, N), vary = variant_of(vy, N);
-    const bool inner = __all_sync(0xffffffffu, !live || (varx == 1 && vary == 1));
-    // row j of the patch: nodes ((vx-1)K + 1 + i, (vy-1)K + 1 + j), interior index (jy - 1) n + (jx - 1)
-    const int64_t g0 = (int64_t(vy - 1) * K + j) * n + int64_t(vx - 1) * K;
-    // the lines live in the per-warp buffer; each contraction walks its input index l at run time (one
-    // buffer load and NP coefficient loads per l), so only the NP accumulators are live
-    T* const row = buf + (p * NP + j) * PR;          // row j of patch p
-    T* const col = buf + p * NP * PR + j;            // column i = j of patch p (stride PR)
-    const bool act = lane < LY::LANES;
-    if (act) {
+    // lane (p, j) holds row j of patch p of each of the G groups
+    bool live[G];
+    int varx[G], vary[G];
+    int64_t g0[G];
+    bool allin = true;
 #pragma unroll
-      for (int i = 0; i < NP; ++i) row[i] = live ? P.r[g0 + i] : T(0);
+    for (int h = 0; h < G; ++h) {
+      const int64_t q = (g * G + h) * PW + p;
+      live[h] = act && q < P.count;
+      int vx = 1, vy = 1;
+      if (live[h]) {
+        const int pid = P.list[q];
+        vy = 1 + pid / Nm1;
+        vx = 1 + (pid - (vy - 1) * Nm1);
+      }
+      varx[h] = variant_of(vx, N);
+      vary[h] = variant_of(vy, N);
+      allin = allin && (!live[h] || (varx[h] == 1 && vary[h] == 1));
+      // row j of the patch: nodes ((vx-1)K + 1 + i, (vy-1)K + 1 + j), interior index (jy - 1) n + (jx - 1)
+      g0[h] = (int64_t(vy - 1) * K + j) * n + int64_t(vx - 1) * K;
     }
-    T o[NP];
+    const bool inner = __all_sync(0xffffffffu, allin);
+    // the lines live in the per-warp buffer; each contraction walks its input index l at run time (one
+    // buffer load per group and NP coefficient loads per l, shared by the G groups on interior warps), so
+    // only the G x NP accumulators are live
+    T* row[G];
+    T* col[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      row[h] = buf + h * LY::GB + (p * NP + j) * PR;        // row j of patch p
+      col[h] = buf + h * LY::GB + p * NP * PR + j;          // column i = j of patch p (stride PR)
+      if (act) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) row[h][i] = live[h] ? P.r[g0[h] + i] : T(0);
+      }
+    }
+    T o[G][NP];
     auto body = [&](auto INC) {
       constexpr bool IN = decltype(INC)::value;
       const Coef2<T, K>& c = coef_at(P.c, round * P.zero);
-      const T* const Sx = IN ? c.S[1] : sS + varx * NP2;
-      const T* const Sy = IN ? c.S[1] : sS + vary * NP2;
-      // S_x^T on row j
+      auto contract = [&](T* const* line, int stride, auto SEL, bool tr) {
+        // o[h][a] = sum_l S_h[l NP + a] line_h[l stride] (tr) or S_h[a NP + l] line_h[l stride]
 #pragma unroll
-      for (int i = 0; i < NP; ++i) o[i] = 0;
+        for (int h = 0; h < G; ++h)
+#pragma unroll
+          for (int a2 = 0; a2 < NP; ++a2) o[h][a2] = 0;
 #pragma unroll 1
-      for (int l = 0; l < NP; ++l) {
-        const T wl = act ? row[l] : T(0);
+        for (int l = 0; l < NP; ++l) {
+          T wl[G];
 #pragma unroll
-        for (int i = 0; i < NP; ++i) o[i] = fma(Sx[l * NP + i], wl, o[i]);
-      }
+          for (int h = 0; h < G; ++h) wl[h] = act ? line[h][l * stride] : T(0);
+          if (IN) {
+#pragma unroll
+            for (int a2 = 0; a2 < NP; ++a2) {
+              const T cf = c.S[1][tr ? l * NP + a2 : a2 * NP + l];
+#pragma unroll
+              for (int h = 0; h < G; ++h) o[h][a2] = fma(cf, wl[h], o[h][a2]);
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+              const T* S = sS + SEL(h) * NP2;
+#pragma unroll
+              for (int a2 = 0; a2 < NP; ++a2) o[h][a2] = fma(S[tr ? l * NP + a2 : a2 * NP + l], wl[h], o[h][a2]);
+            }
+          }
+        }
+      };
+      auto selx = [&](int h) { return varx[h]; };
+      auto sely = [&](int h) { return vary[h]; };
+      // S_x^T on row j
+      contract(row, 1, selx, true);
       if (act) {
 #pragma unroll
-        for (int i = 0; i < NP; ++i) row[i] = o[i];
+        for (int h = 0; h < G; ++h)
+#pragma unroll
+          for (int i = 0; i < NP; ++i) row[h][i] = o[h][i];
       }
       __syncwarp();
       // lane (p, j) now owns column i = j: S_y^T, scale 1 / (lam_x,i + lam_y,jj), S_y
+      contract(col, PR, sely, true);
 #pragma unroll
-      for (int jj = 0; jj < NP; ++jj) o[jj] = 0;
-#pragma unroll 1
-      for (int l = 0; l < NP; ++l) {
-        const T wl = act ? col[l * PR] : T(0);
+      for (int h = 0; h < G; ++h) {
+        // interior patches multiply by the tabulated reciprocal on either path (a patch gives the same bits
+        // whichever warp it lands in: the slab MVS colour lists group patches differently)
+        if (IN || (varx[h] == 1 && vary[h] == 1)) {
 #pragma unroll
-        for (int jj = 0; jj < NP; ++jj) o[jj] = fma(Sy[l * NP + jj], wl, o[jj]);
+          for (int jj = 0; jj < NP; ++jj) o[h][jj] *= tab[j * NP + jj];
+        } else {
+          const T lx = sL[varx[h] * NP + j];
+#pragma unroll
+          for (int jj = 0; jj < NP; ++jj) o[h][jj] *= T(1) / (lx + sL[vary[h] * NP + jj]);
+        }
+        if (act) {                                   // the column is this lane's own: no sync needed
+#pragma unroll
+          for (int jj = 0; jj < NP; ++jj) col[h][jj * PR] = o[h][jj];
+        }
       }
-      if (IN) {
-#pragma unroll
-        for (int jj = 0; jj < NP; ++jj) o[jj] *= tab[j * NP + jj];
-      } else {
-        const T lx = sL[varx * NP + j];
-#pragma unroll
-        for (int jj = 0; jj < NP; ++jj) o[jj] /= (lx + sL[vary * NP + jj]);
-      }
-      if (act) {                                     // the column is this lane's own: no sync needed
-#pragma unroll
-        for (int jj = 0; jj < NP; ++jj) col[jj * PR] = o[jj];
-      }
-#pragma unroll
-      for (int jj = 0; jj < NP; ++jj) o[jj] = 0;
-#pragma unroll 1
-      for (int l = 0; l < NP; ++l) {
-        const T wl = act ? col[l * PR] : T(0);
-#pragma unroll
-        for (int jj = 0; jj < NP; ++jj) o[jj] = fma(Sy[jj * NP + l], wl, o[jj]);
-      }
+      contract(col, PR, sely, false);
       if (act) {
 #pragma unroll
-        for (int jj = 0; jj < NP; ++jj) col[jj * PR] = o[jj];
+        for (int h = 0; h < G; ++h)
+#pragma unroll
+          for (int jj = 0; jj < NP; ++jj) col[h][jj * PR] = o[h][jj];
       }
       __syncwarp();
       // S_x on row j
-#pragma unroll
-      for (int i = 0; i < NP; ++i) o[i] = 0;
-#pragma unroll 1
-      for (int l = 0; l < NP; ++l) {
-        const T wl = act ? row[l] : T(0);
-#pragma unroll
-        for (int i = 0; i < NP; ++i) o[i] = fma(Sx[i * NP + l], wl, o[i]);
-      }
-      __syncwarp();                                  // the buffer is rewritten by the next group
+      contract(row, 1, selx, false);
+      __syncwarp();                                  // the buffer is rewritten by the next iteration
     };
     if (inner) body(std::true_type{});
     else body(std::false_type{});
-    if (live) {
 #pragma unroll
-      for (int i = 0; i < NP; ++i) P.x[g0 + i] = fma(P.factor, o[i], P.x[g0 + i]);
-    }
+    for (int h = 0; h < G; ++h)
+      if (live[h]) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) P.x[g0[h] + i] = fma(P.factor, o[h][i], P.x[g0[h] + i]);
+      }
   }
 }
 
@@ -1322,7 +1352,7 @@ static void launch_list2d(const FusedLevel& F, T omega, const T* r, T* x, const 
   p.r = r; p.x = x; p.list = list; p.count = count; p.N = F.N; p.n = F.n;
   p.factor = T(double(omega) * F.h * F.h);
   p.zero = 0;
-  const int64_t groups = (count + LY::PW - 1) / LY::PW;
+  const int64_t groups = (count + LY::G * LY::PW - 1) / (LY::G * LY::PW);
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(grid_cache, (groups + 7) / 8));
   patch_list2d_kernel<T, K><<<(unsigned)grid, 256, smem, st>>>(p);
 }
