@@ -1139,8 +1139,20 @@ struct Mvs3Layout {
   static constexpr int TOTAL = NW * WARP + TAB;
 };
 
+// kernel parameters: MvsP plus the interior-variant (v = 1) rows of the per-variant tables, so that interior
+// patches (every axis variant 1, warp-uniform: one warp per patch) read their coefficients as uniform
+// kernel-parameter operands instead of one shared-memory load per FMA
 template <typename T, int K>
-__global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP<T, K> P) {
+struct Mvs3P {
+  MvsP<T, K> m;
+  T tB[2 * K - 1][4 * K + 1];
+  T tM[2 * K - 1][2 * K + 1];
+  T tL[2 * K - 1][2 * K + 1];
+};
+
+template <typename T, int K>
+__global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ Mvs3P<T, K> PP) {
+  const MvsP<T, K>& P = PP.m;
   using LY = Mvs3Layout<T, K>;
   constexpr int NP = LY::NP, W = LY::W, F = LY::F, NW = LY::NW;
   constexpr int TB = NP * F, TM = NP * W, TS = NP * NP;
@@ -1190,9 +1202,14 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
   T* const buf = xm;                          // FDM transposes (np^3), Xm is dead by then
   const int Nm1 = int(N - 1);
   const T* __restrict__ X = P.x;
+  // uniform trip count over the CTA (the coefficient offsets of the interior path must be provably uniform)
+  const int64_t pstride = int64_t(gridDim.x) * NW, pfirst = int64_t(blockIdx.x) * NW;
+  const int iters = P.count > pfirst ? int((P.count - pfirst + pstride - 1) / pstride) : 0;
 
 #pragma unroll 1
-  for (int64_t pi = int64_t(blockIdx.x) * NW + warp; pi < P.count; pi += int64_t(gridDim.x) * NW) {
+  for (int round = 0; round < iters; ++round) {
+    const int64_t pi = pfirst + warp + int64_t(round) * pstride;
+    if (pi >= P.count) continue;
     const int pid = P.list[pi];
     const int vx = 1 + pid % Nm1, vy = 1 + (pid / Nm1) % Nm1, vz = 1 + pid / (Nm1 * Nm1);
     const int varx = variant_of(vx, N), vary = variant_of(vy, N), varz = variant_of(vz, N);
@@ -1204,9 +1221,27 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
       if (!inner && (gx < 1 || gx > KN - 1 || gy < 1 || gy > KN - 1 || gz < 1 || gz > KN - 1)) return T(0);
       return __ldg(X + ((gz - 1) * n + (gy - 1)) * n + (gx - 1));
     };
-    const T* bx = Bt + varx * TB;
-    const T* mx = Mt + varx * TM;
-    const T* lx = Lt + varx * TM;
+    auto body = [&](auto INC) {
+    constexpr bool IN = decltype(INC)::value;
+    // coefficient tables: interior patches from the kernel parameters (opaque zero offset per patch: loaded at
+    // the point of use as uniform operands), the others from the shared per-variant copies
+    const Mvs3P<T, K>& Q = *reinterpret_cast<const Mvs3P<T, K>*>(reinterpret_cast<const char*>(&PP) + round * P.zero);
+    const T* bx = Bt + varx * TB; const T* mx = Mt + varx * TM; const T* lx = Lt + varx * TM;
+    const T* by = Bt + vary * TB; const T* my = Mt + vary * TM; const T* ly = Lt + vary * TM;
+    const T* bz = Bt + varz * TB; const T* mz = Mt + varz * TM; const T* lz = Lt + varz * TM;
+    const T* sx = St + varx * TS; const T* sy = St + vary * TS; const T* sz = St + varz * TS;
+    auto bx_ = [&](int i) { return IN ? (&Q.tB[0][0])[i] : bx[i]; };
+    auto by_ = [&](int i) { return IN ? (&Q.tB[0][0])[i] : by[i]; };
+    auto bz_ = [&](int i) { return IN ? (&Q.tB[0][0])[i] : bz[i]; };
+    auto mx_ = [&](int i) { return IN ? (&Q.tM[0][0])[i] : mx[i]; };
+    auto my_ = [&](int i) { return IN ? (&Q.tM[0][0])[i] : my[i]; };
+    auto mz_ = [&](int i) { return IN ? (&Q.tM[0][0])[i] : mz[i]; };
+    auto lx_ = [&](int i) { return IN ? (&Q.tL[0][0])[i] : lx[i]; };
+    auto ly_ = [&](int i) { return IN ? (&Q.tL[0][0])[i] : ly[i]; };
+    auto lz_ = [&](int i) { return IN ? (&Q.tL[0][0])[i] : lz[i]; };
+    auto sx_ = [&](int i) { return IN ? Q.m.c.S[1][i] : sx[i]; };
+    auto sy_ = [&](int i) { return IN ? Q.m.c.S[1][i] : sy[i]; };
+    auto sz_ = [&](int i) { return IN ? Q.m.c.S[1][i] : sz[i]; };
     // ---- x stage: W x W rows (Xm, Xb, Xl); RB1 rows per lane share every coefficient load
     {
       constexpr int RB1 = cdiv(W * W, 32), L1 = cdiv(W * W, RB1);
@@ -1230,11 +1265,11 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
 #pragma unroll
           for (int j = 0; j < RB1; ++j) ab[j] = am[j] = al[j] = 0;
 #pragma unroll
-          for (int f = 0; f < F; ++f) fma_lines<T, RB1>(bx[p * F + f], w[f], ab);
+          for (int f = 0; f < F; ++f) fma_lines<T, RB1>(bx_(p * F + f), w[f], ab);
 #pragma unroll
           for (int c = 0; c < W; ++c) {
-            fma_lines<T, RB1>(mx[p * W + c], w[K + c], am);
-            fma_lines<T, RB1>(lx[p * W + c], w[K + c], al);
+            fma_lines<T, RB1>(mx_(p * W + c), w[K + c], am);
+            fma_lines<T, RB1>(lx_(p * W + c), w[K + c], al);
           }
 #pragma unroll
           for (int j = 0; j < RB1; ++j) {
@@ -1271,7 +1306,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
 #pragma unroll
           for (int j = 0; j < RB2; ++j) am[j] = 0;
 #pragma unroll
-          for (int c = 0; c < W; ++c) fma_lines<T, RB2>(mx[p * W + c], w[c], am);
+          for (int c = 0; c < W; ++c) fma_lines<T, RB2>(mx_(p * W + c), w[c], am);
 #pragma unroll
           for (int j = 0; j < RB2; ++j)
             if (ok[j]) xm[(rzz[j] * F + ry[j]) * NP + p] = am[j];
@@ -1280,9 +1315,6 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
     }
     __syncwarp();
     // ---- y stage
-    const T* by = Bt + vary * TB;
-    const T* my = Mt + vary * TM;
-    const T* ly = Lt + vary * TM;
 #pragma unroll 1
     for (int l = lane; l < (2 * W + F) * NP; l += 32) {
       const int xq = l % NP, zl = l / NP;
@@ -1300,9 +1332,9 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
         for (int p = 0; p < NP; ++p) {
           T a = 0;
 #pragma unroll
-          for (int c = 0; c < W; ++c) a = fma(my[p * W + c], wb[c], fma(T(2) * ly[p * W + c], wl[c], a));
+          for (int c = 0; c < W; ++c) a = fma(my_(p * W + c), wb[c], fma(T(2) * ly_(p * W + c), wl[c], a));
 #pragma unroll
-          for (int f = 0; f < F; ++f) a = fma(by[p * F + f], wm[f], a);
+          for (int f = 0; f < F; ++f) a = fma(by_(p * F + f), wm[f], a);
           g1[(zl * NP + p) * NP + xq] = a;
         }
       } else if (zl < 2 * W) {                        // G3 on z = K + (zl - W)
@@ -1317,7 +1349,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
         for (int p = 0; p < NP; ++p) {
           T a = 0;
 #pragma unroll
-          for (int c = 0; c < W; ++c) a = fma(my[p * W + c], wl[c], fma(ly[p * W + c], wm[c], a));
+          for (int c = 0; c < W; ++c) a = fma(my_(p * W + c), wl[c], fma(ly_(p * W + c), wm[c], a));
           g3[(z3 * NP + p) * NP + xq] = T(2) * a;
         }
       } else {                                        // G2 on z = zl - 2W in F
@@ -1329,19 +1361,13 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
         for (int p = 0; p < NP; ++p) {
           T a = 0;
 #pragma unroll
-          for (int c = 0; c < W; ++c) a = fma(my[p * W + c], wm[c], a);
+          for (int c = 0; c < W; ++c) a = fma(my_(p * W + c), wm[c], a);
           g2[(z * NP + p) * NP + xq] = a;
         }
       }
     }
     __syncwarp();
     // ---- z stage + residual + S_z^T (lanes <-> (x', y') lines)
-    const T* bz = Bt + varz * TB;
-    const T* mz = Mt + varz * TM;
-    const T* lz = Lt + varz * TM;
-    const T* sx = St + varx * TS;
-    const T* sy = St + vary * TS;
-    const T* sz = St + varz * TS;
     const bool act = lane < NP * NP;
     const int xq = lane % NP, yq = lane / NP;
     const int64_t gx = jx0 + K + 1 + xq, gy = jy0 + K + 1 + yq;     // patch node (global node index)
@@ -1359,9 +1385,9 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
       for (int p = 0; p < NP; ++p) {
         T a = 0;
 #pragma unroll
-        for (int c = 0; c < W; ++c) a = fma(mz[p * W + c], w1[c], fma(lz[p * W + c], w3[c], a));
+        for (int c = 0; c < W; ++c) a = fma(mz_(p * W + c), w1[c], fma(lz_(p * W + c), w3[c], a));
 #pragma unroll
-        for (int f = 0; f < F; ++f) a = fma(bz[p * F + f], w2[f], a);
+        for (int f = 0; f < F; ++f) a = fma(bz_(p * F + f), w2[f], a);
         const int64_t gz = jz0 + K + 1 + p;
         rz[p] = fma(-P.scale, a, P.b[((gz - 1) * n + (gy - 1)) * n + (gx - 1)]);
       }
@@ -1372,7 +1398,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
 #pragma unroll
       for (int l = 0; l < NP; ++l)
 #pragma unroll
-        for (int i = 0; i < NP; ++i) o[i] = fma(sz[l * NP + i], rz[l], o[i]);
+        for (int i = 0; i < NP; ++i) o[i] = fma(sz_(l * NP + i), rz[l], o[i]);
 #pragma unroll
       for (int i = 0; i < NP; ++i) buf[(i * NP + yq) * NP + xq] = o[i];    // buf[z'][y][x]
     }
@@ -1388,7 +1414,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
 #pragma unroll
       for (int l = 0; l < NP; ++l)
 #pragma unroll
-        for (int i = 0; i < NP; ++i) o[i] = fma(sy[l * NP + i], w[l], o[i]);
+        for (int i = 0; i < NP; ++i) o[i] = fma(sy_(l * NP + i), w[l], o[i]);
 #pragma unroll
       for (int i = 0; i < NP; ++i) buf[(zb * NP + i) * NP + xa] = o[i];
     }
@@ -1404,7 +1430,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
 #pragma unroll
       for (int l = 0; l < NP; ++l)
 #pragma unroll
-        for (int i = 0; i < NP; ++i) o[i] = fma(sx[l * NP + i], w[l], o[i]);
+        for (int i = 0; i < NP; ++i) o[i] = fma(sx_(l * NP + i), w[l], o[i]);
       const T lyz = Lam[vary * NP + ya] + Lam[varz * NP + zb];
 #pragma unroll
       for (int i = 0; i < NP; ++i) o[i] = P.factor * o[i] / (Lam[varx * NP + i] + lyz);
@@ -1413,7 +1439,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
 #pragma unroll
       for (int i = 0; i < NP; ++i)
 #pragma unroll
-        for (int l = 0; l < NP; ++l) w[l] = fma(sx[l * NP + i], o[i], w[l]);
+        for (int l = 0; l < NP; ++l) w[l] = fma(sx_(l * NP + i), o[i], w[l]);
 #pragma unroll
       for (int l = 0; l < NP; ++l) buf[(zb * NP + ya) * NP + l] = w[l];
     }
@@ -1429,7 +1455,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
 #pragma unroll
       for (int i = 0; i < NP; ++i)
 #pragma unroll
-        for (int l = 0; l < NP; ++l) o[l] = fma(sy[l * NP + i], w[i], o[l]);
+        for (int l = 0; l < NP; ++l) o[l] = fma(sy_(l * NP + i), w[i], o[l]);
 #pragma unroll
       for (int l = 0; l < NP; ++l) buf[(zb * NP + l) * NP + xa] = o[l];
     }
@@ -1444,7 +1470,7 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
 #pragma unroll
       for (int i = 0; i < NP; ++i)
 #pragma unroll
-        for (int l = 0; l < NP; ++l) o[l] = fma(sz[l * NP + i], w[i], o[l]);
+        for (int l = 0; l < NP; ++l) o[l] = fma(sz_(l * NP + i), w[i], o[l]);
 #pragma unroll
       for (int l = 0; l < NP; ++l) {
         const int64_t gz = jz0 + K + 1 + l;
@@ -1453,6 +1479,11 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ MvsP
       }
     }
     __syncwarp();
+    };
+    // measured: k = 2 MVS step 2.53 -> 3.17 GDoF/s with the parameter-space coefficients, k = 3 2.37 -> 2.22
+    // (158 registers, per-lane LDC), so the shared tables stay at k = 3
+    if (K == 2 && varx == 1 && vary == 1 && varz == 1) body(std::true_type{});
+    else body(std::false_type{});
   }
 }
 
@@ -1471,14 +1502,32 @@ static void launch_mvs3(const FusedLevel& F, const int32_t* list, int64_t count,
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, mvs3d_kernel<T, K>, 128, smem);
     grid_cache = sms * std::max(per, 1);
   }
-  MvsP<T, K> p;
+  Mvs3P<T, K> pp;
+  MvsP<T, K>& p = pp.m;
   std::memcpy(&p.c, coef_of<T>(F).data(), sizeof(p.c));
   p.x = x; p.b = b; p.list = list; p.count = count; p.N = F.N; p.n = F.n;
   p.scale = T(1.0 / F.h);                  // 3D: A = h^-1 A^
   p.factor = T(double(omega) * F.h);       //     A~^-1 = h A^~^-1
   p.zero = 0;
+  {   // interior-variant table rows (the kernel's Bt/Mt/Lt[1], representative vertex N/2)
+    constexpr int NP = 2 * K - 1;
+    const int64_t vr = F.N / 2;
+    for (int q = 0; q < NP; ++q) {
+      const int64_t jo = (vr - 1) * K + 1 + q;
+      const int cls = int(jo % K);
+      for (int c = 0; c <= 4 * K; ++c) {
+        const int64_t off = (vr - 2) * K + c - jo;
+        pp.tB[q][c] = (off >= -2 * K && off <= 2 * K) ? p.c.BI[cls][off + 2 * K] : T(0);
+      }
+      for (int c = 0; c <= 2 * K; ++c) {
+        const int64_t off = (vr - 1) * K + c - jo;
+        pp.tM[q][c] = (off >= -K && off <= K) ? p.c.MI[cls][off + K] : T(0);
+        pp.tL[q][c] = (off >= -K && off <= K) ? p.c.LI[cls][off + K] : T(0);
+      }
+    }
+  }
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid_cache, (count + LY::NW - 1) / LY::NW));
-  mvs3d_kernel<T, K><<<grid, 128, smem, st>>>(p);
+  mvs3d_kernel<T, K><<<grid, 128, smem, st>>>(pp);
 }
 
 template <typename T>
