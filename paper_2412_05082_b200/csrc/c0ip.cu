@@ -458,9 +458,13 @@ void disjoint_patch_solve(c0ip_ctx ctx, Level& L, const T* r, T* x, T omega, con
   if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
       c0ip::fused3_patch_fdm<T>(*L.fused, omega, r, x, list, count, st, &ctx->launches))
     return;
+  // 2D lists: patch_list2d, except FP64 k = 3, 4 where the DMMA patch solve is faster (at k = 2 the 3 -> 8
+  // padding of the DMMA fragments makes it the slower one: MVS step 9.9 vs 7.8 GDoF/s measured)
+  const bool fused2 = ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 2;
+  if (fused2 && ctx->k == 2 && c0ip::fused2_patch_list<T>(*L.fused, omega, r, x, list, count, st, &ctx->launches))
+    return;
   if (mma_patches<T>(ctx, L, r, x, omega, list, count, 0, st)) return;
-  if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 2 &&
-      c0ip::fused2_patch_list<T>(*L.fused, omega, r, x, list, count, st, &ctx->launches))
+  if (fused2 && c0ip::fused2_patch_list<T>(*L.fused, omega, r, x, list, count, st, &ctx->launches))
     return;
   patch_solve<T>(ctx, L, r, x, omega, list, count, 0, st);
 }
@@ -1583,15 +1587,8 @@ void slab_mvs_color_impl(c0ip_ctx ctx, Level& L, int color, T omega, int64_t row
         c0ip::fused_apply<T>(*L.fused, x_ext, b_ext, r_ext, st, &ctx->launches, &wr)))
     generic_apply<T>(ctx, L, xv, bv, rv, st, wr.out_lo - 1, wr.out_hi - 1);
   if (ctx->local == C0IP_LOCAL_EXACT) throw std::runtime_error("slab MVS with exact local solvers is not supported");
-  if (mma_patches<T>(ctx, L, rv, xv, omega, list, cnt, 0, st)) return;
-  // 2D k >= 5 (and FP32): the kernel of the single-domain colour step, so the owned rows stay bitwise equal
-  if (fused && c0ip::fused_dim(*L.fused) == 2 &&
-      c0ip::fused2_patch_list<T>(*L.fused, omega, rv, xv, list, cnt, st, &ctx->launches))
-    return;
-  if (ctx->path == C0IP_PATH_AUTO && L.fused && c0ip::fused_dim(*L.fused) == 3 &&
-      c0ip::fused3_patch_fdm<T>(*L.fused, omega, rv, xv, list, cnt, st, &ctx->launches, 0))
-    return;
-  patch_solve<T>(ctx, L, rv, xv, omega, list, cnt, 0, st);
+  // the patch-solve kernel of the single-domain colour step, so the owned rows stay bitwise equal
+  disjoint_patch_solve<T>(ctx, L, rv, xv, omega, list, cnt, st);
 }
 
 // coarse node rows [c_out_lo, c_out_hi) of P^T fine (restriction) from a fine window

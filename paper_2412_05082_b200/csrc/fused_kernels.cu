@@ -1357,14 +1357,16 @@ static void launch_list2d(const FusedLevel& F, T omega, const T* r, T* x, const 
   patch_list2d_kernel<T, K><<<(unsigned)grid, 256, smem, st>>>(p);
 }
 
-// lowest degree at which the 2D MVS colour runs as residual + patch_list2d instead of the fused
-// per-patch kernels (C0IP_MVS2D_SPLIT_K overrides: measurement knob)
-static int mvs2d_split_k() {
-  static const int k = [] {
+// whether the 2D MVS colour runs as residual + patch_list2d instead of the fused per-patch kernels:
+// k = 2 and k >= 5 (measured MVS step: k = 2 9.9 vs 7.8 GDoF/s for mvs2d_mma, whose 8x8 fragments pad the
+// 3-point patch lines; k = 3, 4: 7.7 / 8.7 vs 13.6 / 14.4); C0IP_MVS2D_SPLIT_K = m splits exactly k >= m
+// (measurement knob)
+static bool mvs2d_split(int k) {
+  static const int m = [] {
     const char* e = std::getenv("C0IP_MVS2D_SPLIT_K");
-    return e ? std::atoi(e) : 5;
+    return e ? std::atoi(e) : 0;
   }();
-  return k;
+  return m > 0 ? k >= m : (k == 2 || k >= 5);
 }
 
 template <typename T>
@@ -1391,7 +1393,7 @@ bool fused_mvs_color(FusedLevel& F, const int32_t* list, int64_t count, T omega,
                      int64_t* launches) {
   if (F.d != 2) return false;
   if (count == 0) return true;
-  if (F.k >= mvs2d_split_k()) return false;     // caller: residual + fused2_patch_list per colour
+  if (mvs2d_split(F.k)) return false;          // caller: residual + fused2_patch_list per colour
   if constexpr (std::is_same<T, double>::value) {
     if (mma_mvs2d(F, list, count, double(omega), b, x, st)) {
       (*launches)++;
