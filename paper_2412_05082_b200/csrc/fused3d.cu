@@ -1231,14 +1231,15 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ Mvs3
     const T* bz = Bt + varz * TB; const T* mz = Mt + varz * TM; const T* lz = Lt + varz * TM;
     const T* sx = St + varx * TS; const T* sy = St + vary * TS; const T* sz = St + varz * TS;
     auto bx_ = [&](int i) { return IN ? (&Q.tB[0][0])[i] : bx[i]; };
-    auto by_ = [&](int i) { return IN ? (&Q.tB[0][0])[i] : by[i]; };
-    auto bz_ = [&](int i) { return IN ? (&Q.tB[0][0])[i] : bz[i]; };
+    constexpr bool INYZ = IN && K == 2;            // k = 3: y / z stages keep the shared tables (registers)
+    auto by_ = [&](int i) { return INYZ ? (&Q.tB[0][0])[i] : by[i]; };
+    auto bz_ = [&](int i) { return INYZ ? (&Q.tB[0][0])[i] : bz[i]; };
     auto mx_ = [&](int i) { return IN ? (&Q.tM[0][0])[i] : mx[i]; };
-    auto my_ = [&](int i) { return IN ? (&Q.tM[0][0])[i] : my[i]; };
-    auto mz_ = [&](int i) { return IN ? (&Q.tM[0][0])[i] : mz[i]; };
+    auto my_ = [&](int i) { return INYZ ? (&Q.tM[0][0])[i] : my[i]; };
+    auto mz_ = [&](int i) { return INYZ ? (&Q.tM[0][0])[i] : mz[i]; };
     auto lx_ = [&](int i) { return IN ? (&Q.tL[0][0])[i] : lx[i]; };
-    auto ly_ = [&](int i) { return IN ? (&Q.tL[0][0])[i] : ly[i]; };
-    auto lz_ = [&](int i) { return IN ? (&Q.tL[0][0])[i] : lz[i]; };
+    auto ly_ = [&](int i) { return INYZ ? (&Q.tL[0][0])[i] : ly[i]; };
+    auto lz_ = [&](int i) { return INYZ ? (&Q.tL[0][0])[i] : lz[i]; };
     auto sx_ = [&](int i) { return IN ? Q.m.c.S[1][i] : sx[i]; };
     auto sy_ = [&](int i) { return IN ? Q.m.c.S[1][i] : sy[i]; };
     auto sz_ = [&](int i) { return IN ? Q.m.c.S[1][i] : sz[i]; };
@@ -1480,9 +1481,10 @@ __global__ void __launch_bounds__(128) mvs3d_kernel(const __grid_constant__ Mvs3
     }
     __syncwarp();
     };
-    // measured: k = 2 MVS step 2.53 -> 3.17 GDoF/s with the parameter-space coefficients, k = 3 2.37 -> 2.22
-    // (158 registers, per-lane LDC), so the shared tables stay at k = 3
-    if (K == 2 && varx == 1 && vary == 1 && varz == 1) body(std::true_type{});
+    // measured MVS step: k = 2 2.53 -> 3.17 GDoF/s with the parameter-space coefficients in every stage; k = 3
+    // 2.37 -> 2.22 with them in every stage (158 registers), 2.52 with them in the x-stage and the S contractions
+    // only (INYZ)
+    if (varx == 1 && vary == 1 && varz == 1) body(std::true_type{});
     else body(std::false_type{});
   }
 }
